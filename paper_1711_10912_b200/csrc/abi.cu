@@ -1,0 +1,338 @@
+// abi.cu -- extern "C" entry points of libtlb200.so (include/tensorlib_b200.h).
+//
+// Argument checks mirror the reference's errors (contraction.py:123-127,
+// 212-222; elementwise.py:69-70; hopm.py:79-97) and return TL_EINVAL so
+// the Python layer raises ValueError with the same meaning.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+#include "tl_common.cuh"
+
+namespace tl {
+
+int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
+                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st);
+int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
+                     int m0, cudaStream_t st);
+int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
+                     int m0, cudaStream_t st);
+size_t reduce_workspace_bytes();
+int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const void *b_ptr, void *result,
+                   bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st);
+int hopm_workspace(const tl_desc &a, size_t *bytes);
+int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, double *const *u, int32_t max_sweeps,
+                 double tol, double *l,
+                 double *hist, int32_t *info, void *ws, size_t ws_bytes, cudaStream_t st);
+int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_ptr, cudaStream_t st);
+
+static thread_local std::string g_error = "no error";
+
+void set_error(const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_error = buf;
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return TL_OK;
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return TL_ECUDA;
+}
+
+const DeviceInfo &device_info() {
+    static std::mutex mu;
+    static std::vector<DeviceInfo> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &d : cache)
+        if (d.device == dev) return d;
+    DeviceInfo d{};
+    d.device = dev;
+    cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (d.num_sms <= 0) d.num_sms = 148;
+    cache.push_back(d);
+    return cache.back();
+}
+
+static bool check_desc(const tl_desc *d, const char *what) {
+    if (d == nullptr) {
+        set_error("%s: null descriptor", what);
+        return false;
+    }
+    if (d->order < 1 || d->order > TL_MAX_ORDER) {
+        set_error("%s: order %d out of range 1..%d", what, d->order, TL_MAX_ORDER);
+        return false;
+    }
+    if (d->dtype != TL_F32 && d->dtype != TL_F64 && d->dtype != TL_I64) {
+        set_error("%s: unknown dtype %d", what, d->dtype);
+        return false;
+    }
+    for (int r = 0; r < d->order; ++r) {
+        if (d->extent[r] < 1) {
+            set_error("%s: extents must be positive", what);
+            return false;
+        }
+        if (d->stride[r] < 0) {
+            set_error("%s: negative strides are not supported", what);
+            return false;
+        }
+    }
+    return true;
+}
+
+static bool is_first_order_dense(const tl_desc &d) {
+    int64_t run = 1;
+    for (int r = 0; r < d.order; ++r) {
+        if (d.extent[r] > 1 && d.stride[r] != run) return false;
+        run *= d.extent[r];
+    }
+    return true;
+}
+
+static bool is_float(int32_t dt) { return dt == TL_F32 || dt == TL_F64; }
+
+}  // namespace tl
+
+using namespace tl;
+
+extern "C" {
+
+int32_t tl_abi_version(void) { return TL_ABI_VERSION; }
+
+int32_t tl_device_arch(void) {
+#if defined(TL_ARCH)
+    return TL_ARCH;
+#else
+    return 100;
+#endif
+}
+
+const char *tl_last_error(void) { return g_error.c_str(); }
+
+int tl_ttv(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr, const tl_desc *c, void *c_ptr,
+           int32_t mode, void *stream) {
+    if (!check_desc(a, "ttv A") || !check_desc(b, "ttv vector") || !check_desc(c, "ttv C")) return TL_EINVAL;
+    const int p = a->order;
+    if (p < 2) {
+        set_error("ttv requires order >= 2, got %d", p);
+        return TL_EINVAL;
+    }
+    if (mode < 1 || mode > p) {
+        set_error("mode %d out of range 1..%d", mode, p);
+        return TL_EINVAL;
+    }
+    // vector: order 1, or an (n, 1) column (contraction.py:58-69)
+    if (!(b->order == 1 || (b->order == 2 && b->extent[1] == 1))) {
+        set_error("ttv vector must be a vector");
+        return TL_EINVAL;
+    }
+    if (b->extent[0] != a->extent[mode - 1]) {
+        set_error("ttv vector length %lld does not match extent %lld", (long long)b->extent[0],
+                  (long long)a->extent[mode - 1]);
+        return TL_EINVAL;
+    }
+    if (c->order != p - 1 || !is_first_order_dense(*c) || c->offset != 0) {
+        set_error("ttv: output must be dense first-order of order p-1");
+        return TL_EINVAL;
+    }
+    for (int r = 0, q = 0; r < p; ++r) {
+        if (r == mode - 1) continue;
+        if (c->extent[q++] != a->extent[r]) {
+            set_error("ttv: output shape mismatch");
+            return TL_EINVAL;
+        }
+    }
+    if (is_float(a->dtype) != is_float(b->dtype) || is_float(a->dtype) != is_float(c->dtype)) {
+        set_error("ttv: mixed integer/floating operands");
+        return TL_EUNSUPPORTED;
+    }
+    const void *bp = (const unsigned char *)b_ptr + b->offset * (int64_t)dtype_size(b->dtype);
+    return ttv_enqueue(*a, a_ptr, bp, b->dtype, b->stride[0], c->dtype, c_ptr, mode - 1, nullptr,
+                       (cudaStream_t)stream);
+}
+
+int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr, const tl_desc *c, void *c_ptr,
+           int32_t mode, void *stream) {
+    if (!check_desc(a, "ttm A") || !check_desc(bmat, "ttm matrix") || !check_desc(c, "ttm C")) return TL_EINVAL;
+    const int p = a->order;
+    if (p < 2) {
+        set_error("ttm requires order >= 2, got %d", p);
+        return TL_EINVAL;
+    }
+    if (mode < 1 || mode > p) {
+        set_error("mode %d out of range 1..%d", mode, p);
+        return TL_EINVAL;
+    }
+    if (bmat->order != 2) {
+        set_error("ttm matrix must have order 2, got %d", bmat->order);
+        return TL_EINVAL;
+    }
+    if (bmat->extent[1] != a->extent[mode - 1]) {
+        set_error("matrix columns %lld do not match extent %lld of mode %d", (long long)bmat->extent[1],
+                  (long long)a->extent[mode - 1], mode);
+        return TL_EINVAL;
+    }
+    if (c->order != p || !is_first_order_dense(*c) || c->offset != 0) {
+        set_error("ttm: output must be dense first-order of order p");
+        return TL_EINVAL;
+    }
+    for (int r = 0; r < p; ++r) {
+        const int64_t want = (r == mode - 1) ? bmat->extent[0] : a->extent[r];
+        if (c->extent[r] != want) {
+            set_error("ttm: output shape mismatch");
+            return TL_EINVAL;
+        }
+    }
+    if (bmat->dtype != a->dtype || c->dtype != a->dtype) {
+        set_error("ttm: A, B and C must share a dtype");
+        return TL_EUNSUPPORTED;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (a->dtype == TL_F64) {
+        int rc = ttm_dmma_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+        if (rc != TL_EUNSUPPORTED) return rc;
+    }
+    return ttm_simt_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+}
+
+size_t tl_reduce_workspace_bytes(void) { return reduce_workspace_bytes(); }
+
+static bool same_shape(const tl_desc &a, const tl_desc &b) {
+    if (a.order != b.order) return false;
+    for (int r = 0; r < a.order; ++r)
+        if (a.extent[r] != b.extent[r]) return false;
+    return true;
+}
+
+int tl_inner(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr, void *result_dev, void *ws,
+             size_t ws_bytes, void *stream) {
+    if (!check_desc(a, "inner A") || !check_desc(b, "inner B")) return TL_EINVAL;
+    if (!same_shape(*a, *b)) {
+        set_error("shape mismatch");
+        return TL_EINVAL;
+    }
+    return reduce_enqueue(*a, a_ptr, *b, b_ptr, result_dev, false, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int tl_frobenius_norm(const tl_desc *a, const void *a_ptr, double *result_dev, void *ws, size_t ws_bytes,
+                      void *stream) {
+    if (!check_desc(a, "norm A")) return TL_EINVAL;
+    if (!is_float(a->dtype)) {
+        set_error("frobenius_norm requires floating elements");
+        return TL_EUNSUPPORTED;
+    }
+    return reduce_enqueue(*a, a_ptr, *a, a_ptr, result_dev, true, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int tl_hopm_workspace_bytes(const tl_desc *a, size_t *ws_bytes) {
+    if (!check_desc(a, "hopm A") || ws_bytes == nullptr) return TL_EINVAL;
+    return hopm_workspace(*a, ws_bytes);
+}
+
+static int hopm_check(const tl_desc *a, double *const *u_ptrs, int32_t max_sweeps) {
+    if (!check_desc(a, "hopm A")) return TL_EINVAL;
+    if (max_sweeps < 1) {
+        set_error("max_sweeps must be >= 1");
+        return TL_EINVAL;
+    }
+    if (!is_float(a->dtype)) {
+        set_error("hopm requires floating elements");
+        return TL_EUNSUPPORTED;
+    }
+    if (u_ptrs == nullptr) {
+        set_error("hopm: null vector array");
+        return TL_EINVAL;
+    }
+    if (a->order > 1) {
+        std::vector<int> dims;
+        if (!dense_order(*a, dims)) {
+            set_error("hopm: A must be a dense permutation layout");
+            return TL_EUNSUPPORTED;
+        }
+    }
+    return TL_OK;
+}
+
+int tl_hopm(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs, double *const *u_ptrs,
+            int32_t max_sweeps, double tol, double *l_dev,
+            double *hist_dev, int32_t *info_dev, void *ws, size_t ws_bytes, void *stream) {
+    int rc = hopm_check(a, u_ptrs, max_sweeps);
+    if (rc != TL_OK) return rc;
+    return hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, ws, ws_bytes,
+                        (cudaStream_t)stream);
+}
+
+struct tl_graph_s {
+    cudaGraphExec_t exec;
+};
+
+int tl_hopm_graph_create(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs, double *const *u_ptrs,
+                         int32_t max_sweeps, double tol,
+                         double *l_dev, double *hist_dev, int32_t *info_dev, void *ws, size_t ws_bytes, void *stream,
+                         tl_graph *out) {
+    int rc = hopm_check(a, u_ptrs, max_sweeps);
+    if (rc != TL_OK) return rc;
+    if (out == nullptr) return TL_EINVAL;
+    (void)device_info();  // cache device attributes outside the capture
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t cap = st;
+    bool own = false;
+    if (st == nullptr) {  // the legacy stream cannot be captured
+        cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_status(e, "hopm graph stream");
+        own = true;
+    }
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        if (own) cudaStreamDestroy(cap);
+        return cuda_status(e, "hopm begin capture");
+    }
+    rc = hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, ws, ws_bytes, cap);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+    if (own) cudaStreamDestroy(cap);
+    if (rc != TL_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e2 != cudaSuccess) return cuda_status(e2, "hopm end capture");
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_status(e, "hopm graph instantiate");
+    *out = new tl_graph_s{exec};
+    return TL_OK;
+}
+
+int tl_graph_launch(tl_graph g, void *stream) {
+    if (g == nullptr) return TL_EINVAL;
+    return cuda_status(cudaGraphLaunch(g->exec, (cudaStream_t)stream), "graph launch");
+}
+
+int tl_graph_destroy(tl_graph g) {
+    if (g == nullptr) return TL_OK;
+    cudaError_t e = cudaGraphExecDestroy(g->exec);
+    delete g;
+    return cuda_status(e, "graph destroy");
+}
+
+int tl_copy(const tl_desc *a, const void *a_ptr, const tl_desc *c, void *c_ptr, void *stream) {
+    if (!check_desc(a, "copy A") || !check_desc(c, "copy C")) return TL_EINVAL;
+    if (!same_shape(*a, *c) || a->dtype != c->dtype) {
+        set_error("copy: shape or dtype mismatch");
+        return TL_EINVAL;
+    }
+    return copy_enqueue(*a, a_ptr, *c, c_ptr, (cudaStream_t)stream);
+}
+
+}  // extern "C"

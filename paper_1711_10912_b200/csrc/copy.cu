@@ -1,0 +1,139 @@
+// copy.cu -- C(i) = A(i) between two layouts/stride sets of one shape.
+//
+// Container-layer support for the hot path: relayout (tensor.py:167-184),
+// assign (tensor.py:141-165) and materialising views before a contraction
+// (contraction.py:539-542).  The destination is dense; the source may be
+// any strided view.  Elements are enumerated in the destination's storage
+// order (stores coalesce) and the source offset comes from a digit map of
+// the same index.  When the source's fastest dimension differs from the
+// destination's, a 32x32 shared-memory tile transposes so that both the
+// loads and the stores coalesce.
+#include <algorithm>
+#include <vector>
+
+#include "plan.h"
+#include "tl_common.cuh"
+
+namespace tl {
+
+struct CopyParams {
+    const void *a;
+    void *c;
+    int64_t n;
+    DigitMap amap, cmap;  // linear index (destination storage order) -> offsets
+    // tiled transpose: X = destination's fastest dim, Y = source's fastest
+    int64_t nX, nY, n_rest, a_sX, a_sY, c_sY, tiles_x, tiles_y;
+    DigitMap rest_a, rest_c;
+};
+
+template <class T> __global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyParams P) {
+    const T *a = (const T *)P.a;
+    T *c = (T *)P.c;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P.n; q += stride)
+        c[P.cmap.map((uint32_t)q)] = a[P.amap.map((uint32_t)q)];
+}
+
+template <class T> __global__ void __launch_bounds__(256) copy_tiled_kernel(const __grid_constant__ CopyParams P) {
+    __shared__ T tile[32][33];
+    const T *a = (const T *)P.a;
+    T *c = (T *)P.c;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t per_rest = P.tiles_x * P.tiles_y;
+    const int64_t tiles = per_rest * P.n_rest;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t rest = t / per_rest;
+        const int64_t txy = t - rest * per_rest;
+        const int64_t ty = txy / P.tiles_x;
+        const int64_t tx = txy - ty * P.tiles_x;
+        const int64_t x0 = tx * 32, y0 = ty * 32;
+        const int64_t ra = P.rest_a.map((uint32_t)rest), rc = P.rest_c.map((uint32_t)rest);
+        for (int xr = wid; xr < 32; xr += 8) {  // lanes along Y: source reads coalesce
+            const int64_t x = x0 + xr, y = y0 + lane;
+            if (x < P.nX && y < P.nY) tile[xr][lane] = a[ra + x * P.a_sX + y * P.a_sY];
+        }
+        __syncthreads();
+        for (int yr = wid; yr < 32; yr += 8) {  // lanes along X: destination stores coalesce
+            const int64_t x = x0 + lane, y = y0 + yr;
+            if (x < P.nX && y < P.nY) c[rc + x + y * P.c_sY] = tile[lane][yr];
+        }
+        __syncthreads();
+    }
+}
+
+template <class T> static cudaError_t launch_copy(const CopyParams &P, bool tiled, int grid, cudaStream_t st) {
+    if (tiled)
+        copy_tiled_kernel<T><<<grid, 256, 0, st>>>(P);
+    else
+        copy_kernel<T><<<grid, 256, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_ptr, cudaStream_t st) {
+    std::vector<int> dc;
+    if (!dense_order(c, dc)) {
+        set_error("copy: destination must be dense");
+        return TL_EUNSUPPORTED;
+    }
+    const size_t s = dtype_size(a.dtype);
+    CopyParams P{};
+    P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)s;
+    P.c = (unsigned char *)c_ptr + c.offset * (int64_t)s;
+    P.n = volume(c);
+    if (P.n == 0) return TL_OK;
+    if (P.n > 0xffffffffll) {
+        set_error("copy: more than 2^32 elements");
+        return TL_EUNSUPPORTED;
+    }
+    // source's fastest (smallest |stride|) non-trivial dimension
+    int Y = -1;
+    for (int r = 0; r < a.order; ++r)
+        if (a.extent[r] > 1 && (Y < 0 || a.stride[r] < a.stride[Y])) Y = r;
+    const int X = dc.empty() ? -1 : dc[0];
+    const DeviceInfo &di = device_info();
+    bool tiled = false;
+    int64_t grid;
+    if (X >= 0 && Y >= 0 && X != Y && c.extent[X] >= 8 && c.extent[Y] >= 8) {
+        tiled = true;
+        P.nX = c.extent[X];
+        P.nY = c.extent[Y];
+        P.a_sX = a.stride[X];
+        P.a_sY = a.stride[Y];
+        P.c_sY = c.stride[Y];
+        DigitList ra, rc;
+        for (int r : dc) {
+            if (r == X || r == Y) continue;
+            ra.push_back({c.extent[r], a.stride[r]});
+            rc.push_back({c.extent[r], c.stride[r]});
+        }
+        P.n_rest = 1;
+        for (auto &d : rc) P.n_rest *= d.first;
+        build_map(ra, P.rest_a);
+        build_map(rc, P.rest_c);
+        P.tiles_x = (P.nX + 31) / 32;
+        P.tiles_y = (P.nY + 31) / 32;
+        grid = std::min<int64_t>(P.tiles_x * P.tiles_y * P.n_rest, (int64_t)di.num_sms * 16);
+    } else {
+        DigitList la, lc;
+        for (int r : dc) {
+            // merge digits contiguous in both source and destination
+            if (!lc.empty() && lc.back().first * lc.back().second == c.stride[r] &&
+                la.back().first * la.back().second == a.stride[r]) {
+                lc.back().first *= c.extent[r];
+                la.back().first *= c.extent[r];
+            } else {
+                lc.push_back({c.extent[r], c.stride[r]});
+                la.push_back({c.extent[r], a.stride[r]});
+            }
+        }
+        build_map(la, P.amap);
+        build_map(lc, P.cmap);
+        grid = std::min<int64_t>((P.n + 255) / 256, (int64_t)di.num_sms * 16);
+    }
+    cudaError_t e;
+    if (s == 4) e = launch_copy<float>(P, tiled, (int)grid, st);
+    else e = launch_copy<double>(P, tiled, (int)grid, st);  // f64 and i64 move 8-byte words
+    return cuda_status(e, "copy launch");
+}
+
+}  // namespace tl

@@ -1,0 +1,243 @@
+// hopm.cu -- device-resident higher-order power method (hopm.py:63-120).
+//
+// The reference's sweep is, for r = 1..p:
+//   w = times_vectors(A, u, skip=r)   -- ttvs over modes p..r+1, r-1..1
+//   norm = frobenius_norm(w); degenerate if 0; l[r] = norm; u[r] = w / norm
+// then lambda = l[p], history, early stop when |lambda - previous| < tol.
+//
+// Here the whole loop is a fixed launch sequence on one stream (capturable
+// into one CUDA graph): no host synchronisation per sweep.  Convergence and
+// degeneracy set a device stop flag that turns every later kernel into a
+// no-op, reproducing the reference's `break` / raise.
+//
+// Exactness with two passes over A per sweep.  times_vectors contracts the
+// highest modes first, so mode r's chain starts with
+//   P_{r+1} = A x_p u_p x_{p-1} ... x_{r+1} u_{r+1},
+// and u_{r+1..p} do not change between mode 1 and mode r within a sweep
+// (Gauss-Seidel updates them later).  Mode 1's chain computes every P_k; the
+// middle modes reuse them and only mode p re-reads A.  The reused tensors
+// are the same deterministic ttv of the same inputs, so the result is
+// bit-identical to the reference while A (the only large operand) is read
+// twice per sweep instead of p times.  The norm of each 1-D w is the
+// reference's sequential fold done by one thread; u = w / norm uses IEEE
+// division -- so lambda history and vectors match the reference bit for bit.
+#include <vector>
+
+#include "plan.h"
+#include "tl_common.cuh"
+
+namespace tl {
+
+int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
+                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st);
+
+struct HopmCtl {
+    int32_t stop;
+    int32_t have_prev;
+    double prev;
+};
+
+constexpr int kNormSmem = 6000;  // doubles staged in shared memory for the norm fold
+
+// Source of w: a float64 buffer, or (order-1 hopm) the tensor itself.
+struct WSource {
+    const void *ptr;
+    int32_t dtype;
+    int64_t stride;
+};
+
+__device__ __forceinline__ double w_at(const WSource &w, int64_t i) {
+    if (w.dtype == TL_F32) return (double)((const float *)w.ptr)[i * w.stride];
+    return ((const double *)w.ptr)[i * w.stride];
+}
+
+__global__ void __launch_bounds__(256) hopm_normalize_kernel(WSource w, int64_t n, double *u, double *l, int r, int p,
+                                                             double *hist, int32_t *info, HopmCtl *ctl, int sweep,
+                                                             double tol) {
+    __shared__ double ws[kNormSmem];
+    __shared__ double nrm;
+    if (*(volatile int32_t *)&ctl->stop) return;
+    const bool staged = n <= kNormSmem;
+    if (staged) {
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) ws[i] = w_at(w, i);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        // frobenius_norm(w) = sqrt(0 + w0*w0 + w1*w1 + ...) in order
+        double acc = 0.0;
+        if (staged) {
+            for (int64_t i = 0; i < n; ++i) acc = fold_step(acc, ws[i], ws[i]);
+        } else {
+            for (int64_t i = 0; i < n; ++i) {
+                const double x = w_at(w, i);
+                acc = fold_step(acc, x, x);
+            }
+        }
+        const double s = __dsqrt_rn(acc);
+        nrm = s;
+        if (s == 0.0) {
+            info[2] = sweep;  // DegenerateInputError(sweep, mode), hopm.py:107-108
+            info[3] = r + 1;
+            info[0] = sweep - 1;
+            ctl->stop = 1;
+        } else {
+            l[r] = s;
+        }
+    }
+    __syncthreads();
+    const double s = nrm;
+    if (s == 0.0) return;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) u[i] = __ddiv_rn(staged ? ws[i] : w_at(w, i), s);
+    if (r == p - 1 && threadIdx.x == 0) {
+        info[0] = sweep;
+        hist[sweep - 1] = s;  // lambda = l[-1], hopm.py:112-113
+        if (ctl->have_prev && fabs(s - ctl->prev) < tol) {
+            info[1] = 1;  // converged, hopm.py:116-118
+            ctl->stop = 1;
+        }
+        ctl->prev = s;
+        ctl->have_prev = 1;
+    }
+}
+
+static tl_desc first_order_desc(int p, const int64_t *shape, int32_t dtype) {
+    tl_desc d{};
+    d.order = p;
+    d.dtype = dtype;
+    d.offset = 0;
+    int64_t run = 1;
+    for (int r = 0; r < p; ++r) {
+        d.extent[r] = shape[r];
+        d.stride[r] = run;
+        run *= shape[r];
+    }
+    return d;
+}
+
+struct HopmLayout {
+    size_t ctl_off;
+    std::vector<size_t> P_off;  // P_k for k = 2..p at index k
+    size_t ping_off, pong_off;
+    size_t total;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static HopmLayout hopm_layout(const tl_desc &a) {
+    const int p = a.order;
+    HopmLayout L;
+    size_t off = 0;
+    L.ctl_off = off;
+    off += 256;
+    L.P_off.assign(p + 2, 0);
+    // P_k (dims 1..k-1) for k = 2..p
+    for (int k = 2; k <= p; ++k) {
+        int64_t sz = 1;
+        for (int r = 0; r < k - 1; ++r) sz *= a.extent[r];
+        L.P_off[k] = off;
+        off += align256((size_t)sz * 8);
+    }
+    // ping-pong for the chains of modes 2..p: largest intermediate
+    int64_t mx = 1;
+    for (int r = 2; r <= p; ++r) {
+        // mode r starts from P_{r+1} (dims 1..r) or A (r == p), contracts r-1..1
+        std::vector<int64_t> dims;
+        for (int s = 0; s < r; ++s) dims.push_back(a.extent[s]);
+        if (r == p) dims.assign(a.extent, a.extent + p);
+        for (int k = r - 1; k >= 1; --k) {
+            dims.erase(dims.begin() + (k - 1));
+            int64_t sz = 1;
+            for (auto d : dims) sz *= d;
+            mx = std::max(mx, sz);
+        }
+    }
+    L.ping_off = off;
+    off += align256((size_t)mx * 8);
+    L.pong_off = off;
+    off += align256((size_t)mx * 8);
+    L.total = off;
+    return L;
+}
+
+int hopm_workspace(const tl_desc &a, size_t *bytes) {
+    *bytes = hopm_layout(a).total;
+    return TL_OK;
+}
+
+int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, double *const *u, int32_t max_sweeps,
+                 double tol, double *l, double *hist, int32_t *info, void *ws, size_t ws_bytes, cudaStream_t st) {
+    const int p = a.order;
+    HopmLayout L = hopm_layout(a);
+    if (ws == nullptr || ws_bytes < L.total) {
+        set_error("hopm: workspace of %zu bytes required", L.total);
+        return TL_EWORKSPACE;
+    }
+    unsigned char *base = (unsigned char *)ws;
+    HopmCtl *ctl = (HopmCtl *)(base + L.ctl_off);
+    cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(HopmCtl), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), st);
+    for (int r = 0; u0 != nullptr && r < p && e == cudaSuccess; ++r)
+        e = cudaMemcpyAsync(u[r], u0[r], (size_t)a.extent[r] * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "hopm init");
+    const int32_t *stop = &ctl->stop;
+    double *ping = (double *)(base + L.ping_off), *pong = (double *)(base + L.pong_off);
+
+    for (int sweep = 1; sweep <= max_sweeps; ++sweep) {
+        for (int r = 0; r < p; ++r) {
+            WSource wsrc{};
+            const int64_t n = a.extent[r];
+            if (p == 1) {
+                // times_vectors with no vectors is a copy of A (contraction.py:504-507)
+                wsrc.ptr = (const unsigned char *)a_ptr + a.offset * (int64_t)dtype_size(a.dtype);
+                wsrc.dtype = a.dtype;
+                wsrc.stride = a.stride[0];
+            } else {
+                // start of the chain: A, or the cached prefix P_{r+2} (one-based r+1 < p)
+                const void *cur_ptr;
+                tl_desc cur;
+                int first_k;  // next (one-based) mode to contract
+                const int mode1 = r + 1;
+                if (mode1 == 1 || mode1 == p) {
+                    cur = a;
+                    cur_ptr = a_ptr;
+                    first_k = (mode1 == 1) ? p : p - 1;
+                } else {
+                    int64_t shp[TL_MAX_ORDER];
+                    for (int s = 0; s < mode1; ++s) shp[s] = a.extent[s];
+                    cur = first_order_desc(mode1, shp, TL_F64);
+                    cur_ptr = base + L.P_off[mode1 + 1];
+                    first_k = mode1 - 1;
+                }
+                bool use_ping = true;
+                for (int k = first_k; k >= 1; --k) {
+                    if (k == mode1) continue;
+                    // output: cur with dimension k removed, first-order float64
+                    int64_t shp[TL_MAX_ORDER];
+                    int q = 0;
+                    for (int s = 0; s < cur.order; ++s)
+                        if (s != k - 1) shp[q++] = cur.extent[s];
+                    void *out;
+                    if (mode1 == 1) {
+                        out = base + L.P_off[k];  // P_k: dims 1..k-1
+                    } else {
+                        out = use_ping ? (void *)ping : (void *)pong;
+                        use_ping = !use_ping;
+                    }
+                    int rc = ttv_enqueue(cur, cur_ptr, u[k - 1], TL_F64, 1, TL_F64, out, k - 1, stop, st);
+                    if (rc != TL_OK) return rc;
+                    cur = first_order_desc(q, shp, TL_F64);
+                    cur_ptr = out;
+                }
+                wsrc.ptr = cur_ptr;
+                wsrc.dtype = TL_F64;
+                wsrc.stride = 1;
+            }
+            hopm_normalize_kernel<<<1, 256, 0, st>>>(wsrc, n, u[r], l, r, p, hist, info, ctl, sweep, tol);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_status(e, "hopm normalize");
+        }
+    }
+    return TL_OK;
+}
+
+}  // namespace tl

@@ -1,0 +1,385 @@
+// reduce.cu -- inner product and Frobenius norm on sm_100a.
+//
+// Reference: inner_product_tensors -> inner_product_flat(a, b, 0)
+// (contraction.py:457-459, elementwise.py:411-433) folds a[i] * b[i] over
+// the shared multi-index; frobenius_norm = sqrt(inner(a, a))
+// (contraction.py:462-464).  A whole-tensor fold cannot stay sequential on
+// a GPU, so these kernels are the one place where results are not
+// bit-identical to the reference: every product is formed exactly
+// (TwoProd via FMA for float64; float32 products are exact in binary64)
+// and summed in double-double (TwoSum) per thread, per warp, per CTA and
+// across CTAs in a fixed order -- accurate to ~1 ulp of the true sum and
+// deterministic run to run.  The reference's own sequential fold carries
+// rounding error of order N eps sum|a b|; parity is therefore checked
+// against |delta| <= rtol * sum|a_i b_i| (tests/).
+//
+// Kernels (all HBM-bound, persistent grid = a multiple of the SM count):
+//   dot_rows   -- a and b share their fastest dimension: rows of
+//                 contiguous elements (a flat same-layout buffer is one
+//                 row); 128-bit streaming loads.
+//   dot_tiled  -- a's and b's fastest dimensions differ (e.g. first-order
+//                 x last-order): 32x32 tiles, b staged through padded
+//                 shared memory so both operands are read coalesced.
+// The last CTA to finish (atomic ticket) combines the per-CTA partials and
+// resets the ticket, so the workspace stays zeroed for graph replay.
+#include <cstdio>
+#include <numeric>
+#include <type_traits>
+#include <vector>
+
+#include "plan.h"
+#include "tl_common.cuh"
+
+namespace tl {
+
+constexpr int kMaxPartials = 148 * 8;
+
+struct DD {  // double-double accumulator
+    double hi, lo;
+};
+
+__device__ __forceinline__ void two_sum_add(DD &acc, double x) {
+    const double s = acc.hi + x;
+    const double bp = s - acc.hi;
+    const double err = (acc.hi - (s - bp)) + (x - bp);
+    acc.hi = s;
+    acc.lo += err;
+}
+__device__ __forceinline__ void dd_add_prod(DD &acc, double a, double b) {
+    const double p = a * b;
+    const double e = fma(a, b, -p);  // exact product error
+    two_sum_add(acc, p);
+    acc.lo += e;
+}
+__device__ __forceinline__ DD dd_merge(DD x, DD y) {
+    DD r = x;
+    two_sum_add(r, y.hi);
+    r.lo += y.lo;
+    return r;
+}
+
+struct Acc64 {  // exact int64 accumulator (mod 2^64)
+    int64_t v;
+};
+
+template <class T> struct RedAcc { using type = DD; };
+template <> struct RedAcc<int64_t> { using type = Acc64; };
+
+__device__ __forceinline__ void acc_zero(DD &a) { a.hi = 0.0; a.lo = 0.0; }
+__device__ __forceinline__ void acc_zero(Acc64 &a) { a.v = 0; }
+__device__ __forceinline__ void acc_prod(DD &a, double x, double y) { dd_add_prod(a, x, y); }
+__device__ __forceinline__ void acc_prod(Acc64 &a, int64_t x, int64_t y) {
+    a.v = (int64_t)((uint64_t)a.v + (uint64_t)x * (uint64_t)y);
+}
+__device__ __forceinline__ DD acc_merge(DD x, DD y) { return dd_merge(x, y); }
+__device__ __forceinline__ Acc64 acc_merge(Acc64 x, Acc64 y) {
+    return Acc64{(int64_t)((uint64_t)x.v + (uint64_t)y.v)};
+}
+__device__ __forceinline__ DD shfl_down(DD a, int d) {
+    DD r;
+    r.hi = __shfl_down_sync(0xffffffffu, a.hi, d);
+    r.lo = __shfl_down_sync(0xffffffffu, a.lo, d);
+    return r;
+}
+__device__ __forceinline__ Acc64 shfl_down(Acc64 a, int d) {
+    return Acc64{(int64_t)__shfl_down_sync(0xffffffffu, (long long)a.v, d)};
+}
+
+struct ReduceParams {
+    const void *a;
+    const void *b;
+    void *result;  // double* (float operands) or int64_t* (int64 operands)
+    double *partials;
+    unsigned int *ticket;
+    int32_t sqrt_result;
+    int64_t n_rows, row_len;  // dot_rows
+    DigitMap rows_a, rows_b;  // row index -> element offsets
+    // dot_tiled
+    int64_t nX, nY, n_rest;
+    int64_t a_sY, b_sX;  // a's stride along Y, b's stride along X
+    DigitMap rest_a, rest_b;
+    int64_t tiles_x, tiles_y;
+};
+
+// Block-level reduction of one accumulator per thread; returns the CTA sum
+// in thread 0.
+template <class Acc> __device__ Acc block_reduce(Acc v) {
+    __shared__ Acc warp_part[32];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = acc_merge(v, shfl_down(v, d));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) warp_part[wid] = v;
+    __syncthreads();
+    Acc r;
+    acc_zero(r);
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        if (lane < nw) r = warp_part[lane];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) r = acc_merge(r, shfl_down(r, d));
+    }
+    return r;
+}
+
+__device__ __forceinline__ void store_partial(double *partials, int idx, DD v) {
+    partials[2 * idx] = v.hi;
+    partials[2 * idx + 1] = v.lo;
+}
+__device__ __forceinline__ void store_partial(double *partials, int idx, Acc64 v) {
+    ((int64_t *)partials)[2 * idx] = v.v;
+}
+__device__ __forceinline__ DD load_partial(const double *partials, int idx, DD *) {
+    return DD{__ldcg(partials + 2 * idx), __ldcg(partials + 2 * idx + 1)};
+}
+__device__ __forceinline__ Acc64 load_partial(const double *partials, int idx, Acc64 *) {
+    return Acc64{(int64_t)__ldcg((const long long *)partials + 2 * idx)};
+}
+__device__ __forceinline__ void write_result(const ReduceParams &P, DD v) {
+    double r = v.hi + v.lo;
+    if (P.sqrt_result) r = sqrt(r);
+    *(double *)P.result = r;
+}
+__device__ __forceinline__ void write_result(const ReduceParams &P, Acc64 v) {
+    *(int64_t *)P.result = v.v;
+}
+
+// Per-CTA partial -> global; last CTA folds partials in index order.
+template <class Acc> __device__ void finish(const ReduceParams &P, Acc cta) {
+    __shared__ bool am_last;
+    if (threadIdx.x == 0) {
+        store_partial(P.partials, blockIdx.x, cta);
+        __threadfence();
+        const unsigned prev = atomicAdd(P.ticket, 1u);
+        am_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    Acc v;
+    acc_zero(v);
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+        v = acc_merge(v, load_partial(P.partials, i, (Acc *)nullptr));
+    v = block_reduce(v);
+    if (threadIdx.x == 0) {
+        write_result(P, v);
+        *P.ticket = 0u;  // leave the workspace zeroed
+    }
+}
+
+template <class T> __device__ __forceinline__ typename std::conditional<std::is_same<T, int64_t>::value, int64_t, double>::type
+as_acc(T v) {
+    return v;
+}
+
+// ------------------------------------------------------------ dot_rows
+template <class TA, class TB, int VEC>
+__global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ ReduceParams P) {
+    using Acc = typename RedAcc<TA>::type;
+    Acc acc;
+    acc_zero(acc);
+    const TA *a = (const TA *)P.a;
+    const TB *b = (const TB *)P.b;
+    const int64_t L = P.row_len;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (P.n_rows == 1) {
+        // flat: 128-bit loads over the whole buffer
+        const int64_t nv = L / VEC;
+        for (int64_t v = tid; v < nv; v += nthreads) {
+            TA xa[VEC];
+            TB xb[VEC];
+            if constexpr (VEC * sizeof(TA) == 16) {
+                *(uint4 *)xa = __ldcs((const uint4 *)(a + v * VEC));
+            } else {
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) xa[j] = __ldcs(a + v * VEC + j);
+            }
+            if constexpr (VEC * sizeof(TB) == 16) {
+                *(uint4 *)xb = __ldcs((const uint4 *)(b + v * VEC));
+            } else {
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) xb[j] = __ldcs(b + v * VEC + j);
+            }
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc_prod(acc, as_acc(xa[j]), as_acc(xb[j]));
+        }
+        for (int64_t e = nv * VEC + tid; e < L; e += nthreads) acc_prod(acc, as_acc(a[e]), as_acc(b[e]));
+    } else {
+        const int64_t total = P.n_rows * L;
+        for (int64_t e = tid; e < total; e += nthreads) {
+            const int64_t r = e / L;
+            const int64_t c = e - r * L;
+            const int64_t oa = P.rows_a.map((uint32_t)r) + c;
+            const int64_t ob = P.rows_b.map((uint32_t)r) + c;
+            acc_prod(acc, as_acc(a[oa]), as_acc(b[ob]));
+        }
+    }
+    acc = block_reduce(acc);
+    finish(P, acc);
+}
+
+// ------------------------------------------------------------ dot_tiled
+template <class TA, class TB>
+__global__ void __launch_bounds__(256) dot_tiled_kernel(const __grid_constant__ ReduceParams P) {
+    using Acc = typename RedAcc<TA>::type;
+    __shared__ TB tile[32][33];
+    Acc acc;
+    acc_zero(acc);
+    const TA *a = (const TA *)P.a;
+    const TB *b = (const TB *)P.b;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t tiles = P.tiles_x * P.tiles_y * P.n_rest;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t rest = t / (P.tiles_x * P.tiles_y);
+        const int64_t txy = t - rest * (P.tiles_x * P.tiles_y);
+        const int64_t ty = txy / P.tiles_x;
+        const int64_t tx = txy - ty * P.tiles_x;
+        const int64_t x0 = tx * 32, y0 = ty * 32;
+        const int64_t ra = P.rest_a.map((uint32_t)rest), rb = P.rest_b.map((uint32_t)rest);
+        // b tile: coalesced along Y (b's fastest dimension)
+        for (int xr = wid; xr < 32; xr += 8) {
+            const int64_t x = x0 + xr, y = y0 + lane;
+            if (x < P.nX && y < P.nY) tile[xr][lane] = __ldcs(b + rb + x * P.b_sX + y);
+        }
+        __syncthreads();
+        // a: coalesced along X (a's fastest dimension); b from the tile
+        for (int yr = wid; yr < 32; yr += 8) {
+            const int64_t x = x0 + lane, y = y0 + yr;
+            if (x < P.nX && y < P.nY) acc_prod(acc, as_acc(__ldcs(a + ra + x + y * P.a_sY)), as_acc(tile[lane][yr]));
+        }
+        __syncthreads();
+    }
+    acc = block_reduce(acc);
+    finish(P, acc);
+}
+
+// ------------------------------------------------------------ planning
+size_t reduce_workspace_bytes() { return (size_t)kMaxPartials * 2 * sizeof(double) + 256; }
+
+int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const void *b_ptr, void *result,
+                   bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (ws == nullptr || ws_bytes < reduce_workspace_bytes()) {
+        set_error("inner/norm: workspace of %zu bytes required", reduce_workspace_bytes());
+        return TL_EWORKSPACE;
+    }
+    std::vector<int> da, db;
+    if (!dense_order(a, da) || !dense_order(b, db)) {
+        set_error("inner/norm: operands must be dense permutation layouts (materialise views first)");
+        return TL_EUNSUPPORTED;
+    }
+    const DeviceInfo &di = device_info();
+    ReduceParams P{};
+    const size_t sa = dtype_size(a.dtype), sb = dtype_size(b.dtype);
+    P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)sa;
+    P.b = (const unsigned char *)b_ptr + b.offset * (int64_t)sb;
+    P.result = result;
+    P.partials = (double *)ws;
+    P.ticket = (unsigned int *)((unsigned char *)ws + (size_t)kMaxPartials * 2 * sizeof(double));
+    P.sqrt_result = do_sqrt ? 1 : 0;
+    const int64_t N = volume(a);
+    const bool same_fast = da.empty() || db.empty() || da[0] == db[0];
+    const bool is_int = a.dtype == TL_I64;
+    if (is_int != (b.dtype == TL_I64)) {
+        set_error("inner: mixing integer and floating operands is not supported");
+        return TL_EUNSUPPORTED;
+    }
+    cudaError_t e = cudaSuccess;
+    const int threads = 256;
+    if (N == 0) {
+        set_error("inner: empty tensor");
+        return TL_EINVAL;
+    }
+    if (same_fast) {
+        // digits of a's memory order with b's strides; rows along the shared fastest dim
+        DigitList dl;
+        for (int r : da) dl.push_back({a.extent[r], b.stride[r]});
+        DigitList col = collapse(dl);
+        // a's memory index -> b offset is col; split off the row (first digit)
+        int64_t row_len = 1, bstep = 1;
+        if (!col.empty()) {
+            row_len = col[0].first;
+            bstep = col[0].second;
+        }
+        if (bstep != 1) {
+            // same fastest dim must be unit-stride in b too
+            set_error("inner: internal plan error");
+            return TL_EUNSUPPORTED;
+        }
+        // row q of a (dense, memory order) starts at q*row_len; in b its
+        // offset is the mixed-radix map of q over the remaining digits
+        DigitList rb(col.begin() + (col.empty() ? 0 : 1), col.end());
+        P.row_len = row_len;
+        P.n_rows = N / row_len;
+        if (P.n_rows > 0xffffffffll) {
+            set_error("inner: too many rows");
+            return TL_EUNSUPPORTED;
+        }
+        build_map(DigitList{{P.n_rows, row_len}}, P.rows_a);
+        if (!build_map(rb, P.rows_b)) return TL_EUNSUPPORTED;
+        const int64_t work = (P.n_rows == 1) ? N / 4 : N;
+        int64_t grid = std::min<int64_t>((int64_t)di.num_sms * 8, (work + threads - 1) / threads);
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, kMaxPartials));
+        const uintptr_t pa = (uintptr_t)P.a, pb = (uintptr_t)P.b;
+        if (a.dtype == TL_F32 && b.dtype == TL_F32) {
+            if (pa % 16 == 0 && pb % 16 == 0)
+                dot_rows_kernel<float, float, 4><<<(unsigned)grid, threads, 0, st>>>(P);
+            else
+                dot_rows_kernel<float, float, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+        } else if (a.dtype == TL_F64 && b.dtype == TL_F64) {
+            if (pa % 16 == 0 && pb % 16 == 0)
+                dot_rows_kernel<double, double, 2><<<(unsigned)grid, threads, 0, st>>>(P);
+            else
+                dot_rows_kernel<double, double, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+        } else if (a.dtype == TL_F32 && b.dtype == TL_F64) {
+            dot_rows_kernel<float, double, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+        } else if (a.dtype == TL_F64 && b.dtype == TL_F32) {
+            dot_rows_kernel<double, float, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+        } else {
+            if (pa % 16 == 0 && pb % 16 == 0)
+                dot_rows_kernel<int64_t, int64_t, 2><<<(unsigned)grid, threads, 0, st>>>(P);
+            else
+                dot_rows_kernel<int64_t, int64_t, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+        }
+        e = cudaGetLastError();
+    } else {
+        const int X = da[0], Y = db[0];
+        P.nX = a.extent[X];
+        P.nY = a.extent[Y];
+        P.a_sY = a.stride[Y];
+        P.b_sX = b.stride[X];
+        DigitList ra, rb;
+        for (int r : da) {
+            if (r == X || r == Y) continue;
+            ra.push_back({a.extent[r], a.stride[r]});
+            rb.push_back({a.extent[r], b.stride[r]});
+        }
+        // merge digits contiguous in both a and b
+        DigitList ma, mb;
+        for (size_t d = 0; d < ra.size(); ++d) {
+            if (!ma.empty() && ma.back().first * ma.back().second == ra[d].second &&
+                mb.back().first * mb.back().second == rb[d].second) {
+                ma.back().first *= ra[d].first;
+                mb.back().first *= rb[d].first;
+            } else {
+                ma.push_back(ra[d]);
+                mb.push_back(rb[d]);
+            }
+        }
+        P.n_rest = 1;
+        for (auto &dg : ma) P.n_rest *= dg.first;
+        if (!build_map(ma, P.rest_a) || !build_map(mb, P.rest_b) || P.n_rest > 0xffffffffll) return TL_EUNSUPPORTED;
+        P.tiles_x = (P.nX + 31) / 32;
+        P.tiles_y = (P.nY + 31) / 32;
+        const int64_t tiles = P.tiles_x * P.tiles_y * P.n_rest;
+        int64_t grid = std::min<int64_t>(std::min<int64_t>((int64_t)di.num_sms * 8, tiles), kMaxPartials);
+        if (a.dtype == TL_F32 && b.dtype == TL_F32) dot_tiled_kernel<float, float><<<(unsigned)grid, 256, 0, st>>>(P);
+        else if (a.dtype == TL_F64 && b.dtype == TL_F64) dot_tiled_kernel<double, double><<<(unsigned)grid, 256, 0, st>>>(P);
+        else if (a.dtype == TL_F32 && b.dtype == TL_F64) dot_tiled_kernel<float, double><<<(unsigned)grid, 256, 0, st>>>(P);
+        else if (a.dtype == TL_F64 && b.dtype == TL_F32) dot_tiled_kernel<double, float><<<(unsigned)grid, 256, 0, st>>>(P);
+        else dot_tiled_kernel<int64_t, int64_t><<<(unsigned)grid, 256, 0, st>>>(P);
+        e = cudaGetLastError();
+    }
+    return cuda_status(e, "inner/norm launch");
+}
+
+}  // namespace tl

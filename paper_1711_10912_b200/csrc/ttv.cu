@@ -1,0 +1,492 @@
+// ttv.cu -- mode-m tensor-times-vector on sm_100a (contraction.py:113-194).
+//
+// A dense tensor of any permutation layout is A[O][K][I] (plan.h).  Every
+// output C(o, i) = sum_k A[o][k][i] * b[k] is the reference's left fold in
+// k order, starting from 0, with separately rounded binary64 products and
+// sums -- so outputs are bit-identical to the reference for float64 and
+// for float32 storage (widened exactly, rounded once on store).
+//
+// Two regimes, chosen by where the contracted mode sits in the layout:
+//
+//  * strided fibers (I >= 32, "regime B"): one thread per output vector of
+//    VEC consecutive inner indices; loads are coalesced along the inner
+//    block (128-bit, L1 no-allocate), k loop unrolled for memory-level
+//    parallelism, b staged in shared memory.
+//
+//  * contiguous / short-stride fibers (I < 32, "regime S", includes the
+//    contracted-stride-1 case): a persistent CTA streams tiles of R
+//    consecutive [K][I] blocks through a 3-stage cp.async shared-memory
+//    pipeline (k-slabs of Kc rows), with row pitch padded so the per-thread
+//    sequential folds read shared memory without bank conflicts (128-bit
+//    LDS along k when I == 1).  One thread owns each output fold, which is
+//    what keeps the summation order identical to the reference.
+#include <cstdio>
+#include <numeric>
+#include <type_traits>
+
+#include "plan.h"
+#include "tl_common.cuh"
+
+namespace tl {
+
+struct TtvParams {
+    const void *a;
+    const void *b;
+    void *c;
+    const int32_t *stop;  // optional device flag: skip all work when set (HOPM)
+    int64_t b_stride;
+    int32_t b_dtype;
+    int32_t b_smem;  // stage b in shared memory
+    int64_t O, K, I;
+    int32_t ident;
+    DigitMap in_map, out_map;
+    // regime S plan
+    int32_t R;        // [K][I] blocks (rows) per tile
+    int32_t Kc;       // k-slab length
+    int32_t Lp;       // smem row pitch (elements)
+    int32_t nslab;    // ceil(K / Kc)
+    int64_t ntiles;   // ceil(O / R)
+    int32_t opt;      // outputs per thread (regime S)
+    FastDiv I_div;    // divides output slot j -> (row, i)
+    FastDiv pr_div;   // pieces per row, full slab
+    FastDiv pr_tail;  // pieces per row, last slab
+};
+
+// ------------------------------------------------------------- regime B
+template <class TA, int VEC> struct VecLoad;
+template <> struct VecLoad<float, 4> {
+    __device__ static void ld(const float *p, double *v) {
+        float4 x = ld_stream_f4(p);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+};
+template <> struct VecLoad<float, 2> {
+    __device__ static void ld(const float *p, double *v) {
+        float2 x = ld_stream_f2(p);
+        v[0] = x.x; v[1] = x.y;
+    }
+};
+template <> struct VecLoad<float, 1> {
+    __device__ static void ld(const float *p, double *v) { v[0] = ld_stream(p); }
+};
+template <> struct VecLoad<double, 2> {
+    __device__ static void ld(const double *p, double *v) {
+        double2 x = ld_stream_d2(p);
+        v[0] = x.x; v[1] = x.y;
+    }
+};
+template <> struct VecLoad<double, 1> {
+    __device__ static void ld(const double *p, double *v) { v[0] = ld_stream(p); }
+};
+template <> struct VecLoad<int64_t, 2> {
+    __device__ static void ld(const int64_t *p, int64_t *v) {
+        longlong2 x = ld_stream_l2(p);
+        v[0] = x.x; v[1] = x.y;
+    }
+};
+template <> struct VecLoad<int64_t, 1> {
+    __device__ static void ld(const int64_t *p, int64_t *v) { v[0] = ld_stream(p); }
+};
+
+template <class TC, int VEC, class Acc>
+__device__ __forceinline__ void store_outputs(const TtvParams &P, int64_t o, int64_t i0, const Acc *acc) {
+    TC *c = (TC *)P.c;
+    if (P.ident) {
+        TC *dst = c + o * P.I + i0;
+        if constexpr (VEC == 4 && sizeof(TC) == 4) {
+            float4 v = make_float4(narrow<TC>(acc[0]), narrow<TC>(acc[1]), narrow<TC>(acc[2]), narrow<TC>(acc[3]));
+            *(float4 *)dst = v;
+        } else if constexpr (VEC == 2 && std::is_same<TC, double>::value) {
+            *(double2 *)dst = make_double2(acc[0], acc[1]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) dst[j] = narrow<TC>(acc[j]);
+        }
+    } else {
+        const int64_t go = P.out_map.map((uint32_t)o);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) c[go + P.in_map.map((uint32_t)(i0 + j))] = narrow<TC>(acc[j]);
+    }
+}
+
+template <class TA, class TC, int VEC, int U>
+__global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant__ TtvParams P) {
+    using Acc = typename AccOf<TA>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Acc *bs = (Acc *)smem_raw;
+    if (stop_requested(P.stop)) return;
+    const int64_t K = P.K, I = P.I;
+    if (P.b_smem) {
+        for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+            bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+        __syncthreads();
+    }
+    const int64_t IV = I / VEC;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= P.O * IV) return;
+    const int64_t o = gid / IV;
+    const int64_t i0 = (gid - o * IV) * VEC;
+    const TA *pa = (const TA *)P.a + (o * K) * I + i0;
+
+    Acc acc[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] = Acc(0);
+
+    int64_t k = 0;
+    for (; k + U <= K; k += U) {
+        Acc v[U][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) VecLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const Acc bk = P.b_smem ? bs[k + u] : load_elem_as<Acc>(P.b, P.b_dtype, (k + u) * P.b_stride);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[u][j], bk);
+        }
+    }
+    for (; k < K; ++k) {
+        Acc v[VEC];
+        VecLoad<TA, VEC>::ld(pa + k * I, v);
+        const Acc bk = P.b_smem ? bs[k] : load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[j], bk);
+    }
+    store_outputs<TC, VEC>(P, o, i0, acc);
+}
+
+// ------------------------------------------------------------- regime S
+constexpr int kStages = 3;
+constexpr int kMaxOpt = 4;
+
+template <class TA, int G>
+__device__ __forceinline__ void issue_slab(const TtvParams &P, unsigned char *stage, int64_t tile, int slab) {
+    const int64_t o0 = tile * P.R;
+    const int64_t rows64 = P.O - o0 < P.R ? P.O - o0 : P.R;
+    const uint32_t rows = (uint32_t)rows64;
+    const int64_t k0 = (int64_t)slab * P.Kc;
+    const int64_t kc = (P.K - k0 < P.Kc) ? P.K - k0 : P.Kc;
+    const bool tail = (kc != P.Kc);
+    const FastDiv &pr = tail ? P.pr_tail : P.pr_div;
+    const uint32_t pieces_row = pr.d;
+    const uint32_t total = rows * pieces_row;
+    const unsigned char *src0 = (const unsigned char *)((const TA *)P.a + (o0 * P.K + k0) * P.I);
+    const int64_t grow = P.K * P.I * (int64_t)sizeof(TA);  // global row pitch, bytes
+    const uint32_t srow = (uint32_t)P.Lp * (uint32_t)sizeof(TA);  // smem row pitch, bytes
+    for (uint32_t p = threadIdx.x; p < total; p += blockDim.x) {
+        uint32_t r, cpc;
+        pr.divmod(p, r, cpc);
+        cp_async<G>(stage + r * srow + cpc * G, src0 + (int64_t)r * grow + (int64_t)cpc * G);
+    }
+}
+
+template <class TA, class TC, int G, bool VECREAD>
+__global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__ TtvParams P) {
+    using Acc = typename AccOf<TA>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (stop_requested(P.stop)) return;
+    const int64_t K = P.K, I = P.I;
+    // b (as the accumulation type), then kStages row-padded stage buffers
+    Acc *bs = (Acc *)smem_raw;
+    const size_t bbytes = ((size_t)K * sizeof(Acc) + 15) & ~(size_t)15;
+    unsigned char *stages = smem_raw + bbytes;
+    const size_t stage_bytes = (((size_t)P.R * P.Lp * sizeof(TA)) + 15) & ~(size_t)15;
+
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+        bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+
+    const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nitems = my_tiles * P.nslab;
+    auto item_tile = [&](int64_t q) { return (int64_t)blockIdx.x + (q / P.nslab) * gridDim.x; };
+    auto item_slab = [&](int64_t q) { return (int)(q % P.nslab); };
+
+#pragma unroll
+    for (int q = 0; q < kStages - 1; ++q) {
+        if (q < nitems) issue_slab<TA, G>(P, stages + q * stage_bytes, item_tile(q), item_slab(q));
+        cp_async_commit();
+    }
+
+    Acc acc[kMaxOpt];
+#pragma unroll
+    for (int t = 0; t < kMaxOpt; ++t) acc[t] = Acc(0);
+
+    const uint32_t outs_per_tile = (uint32_t)P.R * (uint32_t)I;
+    for (int64_t q = 0; q < nitems; ++q) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        {
+            const int64_t qn = q + kStages - 1;
+            if (qn < nitems) issue_slab<TA, G>(P, stages + (qn % kStages) * stage_bytes, item_tile(qn), item_slab(qn));
+            cp_async_commit();
+        }
+        const TA *st = (const TA *)(stages + (q % kStages) * stage_bytes);
+        const int64_t tile = item_tile(q);
+        const int slab = item_slab(q);
+        const int64_t k0 = (int64_t)slab * P.Kc;
+        const int kc = (int)((K - k0 < P.Kc) ? K - k0 : P.Kc);
+        const int64_t o0 = tile * P.R;
+        const int64_t rows = (P.O - o0 < P.R) ? P.O - o0 : P.R;
+
+#pragma unroll
+        for (int t = 0; t < kMaxOpt; ++t) {
+            if (t >= P.opt) break;
+            const uint32_t j = threadIdx.x + t * blockDim.x;
+            if (j >= outs_per_tile) break;
+            uint32_t r, i;
+            P.I_div.divmod(j, r, i);
+            if (r >= rows) break;
+            const TA *row = st + (size_t)r * P.Lp + i;
+            Acc a_ = acc[t];
+            if constexpr (VECREAD) {
+                // I == 1, 16-byte rows: LDS.128 along k, folds stay in k order
+                constexpr int E = 16 / sizeof(TA);
+                for (int kk = 0; kk < kc; kk += E) {
+                    if constexpr (E == 4) {
+                        const float4 v = *(const float4 *)(row + kk);
+                        a_ = fold_step(a_, (Acc)v.x, bs[k0 + kk + 0]);
+                        a_ = fold_step(a_, (Acc)v.y, bs[k0 + kk + 1]);
+                        a_ = fold_step(a_, (Acc)v.z, bs[k0 + kk + 2]);
+                        a_ = fold_step(a_, (Acc)v.w, bs[k0 + kk + 3]);
+                    } else {
+                        union { uint4 raw; TA v[2]; } u;
+                        u.raw = *(const uint4 *)(row + kk);
+                        a_ = fold_step(a_, (Acc)u.v[0], bs[k0 + kk + 0]);
+                        a_ = fold_step(a_, (Acc)u.v[1], bs[k0 + kk + 1]);
+                    }
+                }
+            } else {
+#pragma unroll 4
+                for (int kk = 0; kk < kc; ++kk) a_ = fold_step(a_, (Acc)row[(size_t)kk * I], bs[k0 + kk]);
+            }
+            acc[t] = a_;
+        }
+
+        if (slab == P.nslab - 1) {
+            TC *c = (TC *)P.c;
+#pragma unroll
+            for (int t = 0; t < kMaxOpt; ++t) {
+                if (t >= P.opt) break;
+                const uint32_t j = threadIdx.x + t * blockDim.x;
+                if (j < outs_per_tile) {
+                    uint32_t r, i;
+                    P.I_div.divmod(j, r, i);
+                    if (r < rows) {
+                        const int64_t o = o0 + r;
+                        int64_t off;
+                        if (P.ident)
+                            off = o * I + i;
+                        else
+                            off = P.out_map.map((uint32_t)o) + P.in_map.map(i);
+                        c[off] = narrow<TC>(acc[t]);
+                    }
+                }
+                acc[t] = Acc(0);
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------- planning
+struct TtvLaunch {
+    TtvParams P;
+    int regime;  // 0 = strided (B), 1 = staged (S)
+    int vec;
+    int G;
+    bool vecread;
+    dim3 grid, block;
+    size_t smem;
+};
+
+static int64_t pow2_divisor(int64_t x) { return x & (-x); }
+
+// Regime-S plan: rows per tile, slab length, pitch, piece size.
+static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
+    TtvParams &P = L.P;
+    const int64_t I = P.I, K = P.K, O = P.O;
+    int threads = 256;
+    int64_t R;
+    if (I == 1) {
+        R = threads;
+        // small problems: fewer rows per tile so every SM gets a tile
+        while (R > 32 && (O + R - 1) / R < nsm) R /= 2;
+        threads = (int)std::max<int64_t>(32, R);
+    } else {
+        R = std::max<int64_t>(1, (int64_t)threads * kMaxOpt / I);
+        while (R > 1 && (O + R - 1) / R < nsm && R * I > 64) R /= 2;
+        threads = (int)std::min<int64_t>(256, std::max<int64_t>(32, ((R * I + 31) / 32) * 32));
+    }
+    // piece size: must divide the global row pitch and the base address
+    int64_t G = 16;
+    while (G > (int64_t)s && (((K * I * s) % G) != 0 || (base_addr % G) != 0)) G /= 2;
+    if (((K * I * s) % G) != 0 || (base_addr % G) != 0) G = s;
+    // slab length: stage ~24 KB
+    const int64_t stage_target = 24 * 1024;
+    int64_t Kc = std::max<int64_t>(1, stage_target / std::max<int64_t>(1, R * I * s));
+    const int64_t g_is = std::gcd(G, I * s);
+    const int64_t unit = G / g_is;  // Kc multiple of unit keeps slab offsets G-aligned
+    if (Kc >= K) {
+        Kc = K;
+    } else {
+        Kc = std::max<int64_t>(unit, Kc - Kc % unit);
+        if (Kc >= K) Kc = K;
+    }
+    const int64_t L0 = Kc * I;
+    int64_t Lp;
+    bool vecread = false;
+    if (I == 1 && G == 16) {
+        vecread = true;
+        Lp = L0;
+        while (((Lp * s) % 16) != 0 || (((Lp * s) / 16) % 2) == 0) ++Lp;
+    } else {
+        const int64_t w = s / 4;            // 32-bit words per element
+        const int64_t M = 32 / w;           // elements per bank cycle
+        const int64_t want = (I == 1) ? 1 : (I % M);
+        Lp = L0;
+        if (I == 1) {
+            if (Lp % 2 == 0) ++Lp;
+        } else {
+            while ((Lp % M) != want) ++Lp;
+        }
+        // keep cp.async destinations G-aligned
+        while (G > s && ((Lp * s) % G) != 0) G /= 2;
+    }
+    const int64_t bbytes = ((K * 8) + 15) & ~15ll;
+    const int64_t stage_bytes = ((R * Lp * s) + 15) & ~15ll;
+    const int64_t smem = bbytes + kStages * stage_bytes;
+    if (smem > 200 * 1024) return false;
+    P.R = (int32_t)R;
+    P.Kc = (int32_t)Kc;
+    P.Lp = (int32_t)Lp;
+    P.nslab = (int32_t)((K + Kc - 1) / Kc);
+    P.ntiles = (O + R - 1) / R;
+    P.opt = (int32_t)((R * I + threads - 1) / threads);
+    if (P.opt > kMaxOpt) return false;
+    P.I_div.init((uint32_t)I);
+    P.pr_div.init((uint32_t)((Kc * I * s) / G));
+    const int64_t ktail = K - (int64_t)(P.nslab - 1) * Kc;
+    P.pr_tail.init((uint32_t)((ktail * I * s) / G));
+    L.regime = 1;
+    L.G = (int)G;
+    L.vecread = vecread;
+    L.block = dim3(threads);
+    L.smem = (size_t)smem;
+    const int per_sm = smem <= 100 * 1024 ? 2 : 1;
+    const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)nsm * per_sm);
+    L.grid = dim3((unsigned)grid);
+    return true;
+}
+
+static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, int32_t a_dtype) {
+    TtvParams &P = L.P;
+    int vec = 1;
+    if (a_dtype == TL_F32) {
+        if (P.I % 4 == 0 && base_addr % 16 == 0) vec = 4;
+        else if (P.I % 2 == 0 && base_addr % 8 == 0) vec = 2;
+    } else {
+        if (P.I % 2 == 0 && base_addr % 16 == 0) vec = 2;
+    }
+    const int64_t nthreads = P.O * (P.I / vec);
+    int threads = 256;
+    while (threads > 32 && (nthreads + threads - 1) / threads < 2 * nsm) threads /= 2;
+    P.b_smem = (P.K <= 8192) ? 1 : 0;
+    L.regime = 0;
+    L.vec = vec;
+    L.block = dim3(threads);
+    L.grid = dim3((unsigned)((nthreads + threads - 1) / threads));
+    L.smem = P.b_smem ? (size_t)P.K * 8 : 0;
+    (void)s;
+    return true;
+}
+
+template <class TA, class TC>
+static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
+    if (L.regime == 0) {
+        constexpr int U = 8;
+        if constexpr (sizeof(TA) == 4) {
+            if (L.vec == 4) {
+                ttv_strided_kernel<TA, TC, 4, U><<<L.grid, L.block, L.smem, st>>>(L.P);
+                return cudaGetLastError();
+            }
+        }
+        if (L.vec == 2) {
+            ttv_strided_kernel<TA, TC, 2, U><<<L.grid, L.block, L.smem, st>>>(L.P);
+        } else {
+            ttv_strided_kernel<TA, TC, 1, U><<<L.grid, L.block, L.smem, st>>>(L.P);
+        }
+        return cudaGetLastError();
+    }
+    auto go = [&](auto kern) -> cudaError_t {
+        if (L.smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<L.grid, L.block, L.smem, st>>>(L.P);
+        return cudaGetLastError();
+    };
+    if (L.vecread) return go(ttv_staged_kernel<TA, TC, 16, true>);
+    switch (L.G) {
+        case 16: return go(ttv_staged_kernel<TA, TC, 16, false>);
+        case 8: return go(ttv_staged_kernel<TA, TC, 8, false>);
+        default:
+            if constexpr (sizeof(TA) == 4) return go(ttv_staged_kernel<TA, TC, 4, false>);
+            return cudaErrorInvalidValue;
+    }
+}
+
+// Entry used by tl_ttv and by the HOPM orchestration (which passes a stop
+// flag and binary64 outputs for float32 storage).
+int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
+                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st) {
+    Canon cn;
+    if (!canon_contraction(a, m0, 0, cn)) {
+        set_error("ttv: operand A is not a dense permutation layout (materialise views first)");
+        return TL_EUNSUPPORTED;
+    }
+    if (cn.O > 0xffffffffll || cn.I > 0xffffffffll || cn.K > 0x7fffffffll) {
+        set_error("ttv: index range exceeds 32-bit digit maps");
+        return TL_EUNSUPPORTED;
+    }
+    const DeviceInfo &di = device_info();
+    TtvLaunch L{};
+    TtvParams &P = L.P;
+    const size_t s = dtype_size(a.dtype);
+    P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)s;
+    P.b = b_ptr;
+    P.c = c_ptr;
+    P.stop = stop;
+    P.b_stride = b_stride;
+    P.b_dtype = b_dtype;
+    P.O = cn.O;
+    P.K = cn.K;
+    P.I = cn.I;
+    P.ident = cn.ident ? 1 : 0;
+    if (!build_map(cn.inner, P.in_map) || !build_map(cn.outer, P.out_map)) {
+        set_error("ttv: extent exceeds 32-bit digit range");
+        return TL_EUNSUPPORTED;
+    }
+    if (P.O * P.I == 0) return TL_OK;
+    const uintptr_t base = (uintptr_t)P.a;
+    bool ok;
+    if (P.I >= 32) {
+        ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
+    } else {
+        ok = plan_staged(L, (int64_t)s, base, di.num_sms);
+        if (!ok) ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
+    }
+    if (!ok) {
+        set_error("ttv: no launch plan");
+        return TL_EUNSUPPORTED;
+    }
+    cudaError_t e;
+    if (a.dtype == TL_F32 && c_dtype == TL_F32) e = launch_typed<float, float>(L, st);
+    else if (a.dtype == TL_F32 && c_dtype == TL_F64) e = launch_typed<float, double>(L, st);
+    else if (a.dtype == TL_F64 && c_dtype == TL_F64) e = launch_typed<double, double>(L, st);
+    else if (a.dtype == TL_I64 && c_dtype == TL_I64) e = launch_typed<int64_t, int64_t>(L, st);
+    else {
+        set_error("ttv: unsupported dtype combination (a=%d, c=%d)", a.dtype, c_dtype);
+        return TL_EUNSUPPORTED;
+    }
+    return cuda_status(e, "ttv launch");
+}
+
+}  // namespace tl

@@ -1,0 +1,166 @@
+"""Higher-order power method on B200 (hopm.py:63-120 of the reference).
+
+The whole Gauss-Seidel loop -- per-mode ttv chains, sequential norms,
+normalisation, lambda history, the tol test and degeneracy -- is one CUDA
+graph built by the C ABI (tl_hopm_graph_create); the host waits once at
+the end.  Results are bit-identical to the reference (csrc/hopm.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _abi
+from .tensor import DenseTensor
+
+__all__ = ["DegenerateInputError", "HopmState", "hopm", "HopmRunner"]
+
+
+class DegenerateInputError(ArithmeticError):
+    """A mode update produced the zero vector (hopm.py:26-35)."""
+
+    def __init__(self, sweep: int, mode: int):
+        super().__init__(f"zero vector at normalization (sweep {sweep}, mode {mode})")
+        self.sweep = sweep
+        self.mode = mode
+
+
+@dataclass
+class HopmState:
+    """u: unit vectors per dimension; l: per-mode norms of the final sweep;
+    scale = l[-1]; histories per sweep (hopm.py:38-56)."""
+
+    u: List[DenseTensor]
+    l: List[float]
+    sweeps: int
+    converged: bool
+    lambda_history: List[float] = field(default_factory=list)
+    residual_history: List[float] = field(default_factory=list)
+
+    @property
+    def scale(self) -> float:
+        return self.l[-1]
+
+
+def _seq_norm(values) -> float:
+    """The reference's frobenius_norm of a vector: sqrt of a left fold."""
+    acc = 0
+    for x in values:
+        acc += x * x
+    return math.sqrt(acc)
+
+
+def _start_vectors(shape, u0) -> List[List[float]]:
+    """hopm.py:81-98, evaluated in host binary64 exactly as the reference
+    does (n ** -0.5, or u0 / frobenius_norm(u0))."""
+    p = len(shape)
+    if u0 is None:
+        return [[n ** -0.5] * n for n in shape]
+    vecs = list(u0)
+    if len(vecs) != p:
+        raise ValueError(f"expected {p} start vectors, got {len(vecs)}")
+    out = []
+    for r, (v, n) in enumerate(zip(vecs, shape), start=1):
+        vshape = tuple(v.shape)
+        if len(vshape) != 1 or vshape != (n,):
+            raise ValueError(f"start vector {r} must have shape ({n},), got {vshape}")
+        vals = [float(x) for x in (v.data if hasattr(v, "data") else v)]
+        nrm = _seq_norm(vals)
+        if nrm == 0.0:
+            raise ValueError(f"start vector {r} is zero")
+        out.append([x / nrm for x in vals])
+    return out
+
+
+class HopmRunner:
+    """A captured HOPM graph over a fixed tensor: ``run()`` replays the
+    whole max_sweeps loop (start vectors are re-copied each replay)."""
+
+    def __init__(self, a: DenseTensor, max_sweeps: int = 50, u0=None, tol: float = 1e-10):
+        if max_sweeps < 1:
+            raise ValueError("max_sweeps must be >= 1")
+        if a.dtype not in (torch.float32, torch.float64):
+            raise NotImplementedError("hopm requires floating elements")
+        self.a = a
+        self.max_sweeps = int(max_sweeps)
+        self.tol = float(tol)
+        dev = a.device
+        starts = _start_vectors(a.shape, u0)
+        self.u0 = [torch.tensor(v, dtype=torch.float64, device=dev) for v in starts]
+        self.u = [torch.empty(len(v), dtype=torch.float64, device=dev) for v in starts]
+        p = a.order
+        self.l = torch.zeros(p, dtype=torch.float64, device=dev)
+        self.hist = torch.zeros(self.max_sweeps, dtype=torch.float64, device=dev)
+        self.info = torch.zeros(4, dtype=torch.int32, device=dev)
+        L = _abi.lib()
+        desc = a.desc()
+        need = ctypes.c_size_t(0)
+        _abi.check(L.tl_hopm_workspace_bytes(desc, ctypes.byref(need)), "hopm workspace")
+        self.ws = torch.zeros(max(int(need.value), 256), dtype=torch.uint8, device=dev)
+        self._u0p = (ctypes.c_void_p * p)(*[t.data_ptr() for t in self.u0])
+        self._up = (ctypes.c_void_p * p)(*[t.data_ptr() for t in self.u])
+        self._graph = ctypes.c_void_p(0)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        rc = L.tl_hopm_graph_create(desc, a.ptr(), self._u0p, self._up, self.max_sweeps, self.tol,
+                                    self.l.data_ptr(), self.hist.data_ptr(), self.info.data_ptr(),
+                                    self.ws.data_ptr(), self.ws.numel(), _abi.stream_handle(self.stream),
+                                    ctypes.byref(self._graph))
+        _abi.check(rc, "hopm graph")
+
+    def launch(self, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.a.device)
+        _abi.check(_abi.lib().tl_graph_launch(self._graph, _abi.stream_handle(s)), "hopm launch")
+
+    def state(self) -> HopmState:
+        info = self.info.cpu().tolist()
+        sweeps, converged, dsweep, dmode = info
+        if dsweep:
+            raise DegenerateInputError(dsweep, dmode)
+        l = self.l.cpu().tolist()
+        hist = self.hist[:sweeps].cpu().tolist()
+        us = [DenseTensor._wrap(_vec_meta(t.numel()), t.clone()) for t in self.u]
+        return HopmState(u=us, l=l, sweeps=sweeps, converged=bool(converged), lambda_history=hist)
+
+    def run(self) -> HopmState:
+        self.launch()
+        return self.state()
+
+    def close(self) -> None:
+        if self._graph:
+            _abi.lib().tl_graph_destroy(self._graph)
+            self._graph = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _vec_meta(n):
+    from .layout import TensorMeta
+
+    return TensorMeta((n,))
+
+
+def hopm(a, max_sweeps: int = 50, u0: Optional[Sequence] = None, tol: float = 1e-10,
+         track_residuals: bool = False) -> HopmState:
+    """Best rank-one approximation by alternating sweeps (hopm.py:63-120).
+
+    Raises DegenerateInputError when a mode update has norm zero, ValueError
+    for max_sweeps < 1 or invalid start vectors."""
+    if max_sweeps < 1:
+        raise ValueError("max_sweeps must be >= 1")
+    if track_residuals:
+        raise NotImplementedError("track_residuals is outside the B200 hot path (hopm.py:142-147)")
+    runner = HopmRunner(a, max_sweeps=max_sweeps, u0=u0, tol=tol)
+    try:
+        return runner.run()
+    finally:
+        runner.close()

@@ -1,0 +1,287 @@
+"""DenseTensor on B200 device memory -- the container of the hot path.
+
+API of the reference container (tensor.py:33-284 of tensorlib): runtime
+shape, one-based layout, offsets; a buffer in memory-index order; outputs
+of contractions are fresh first-order tensors with zero offsets.  What
+differs, by design:
+
+* the buffer is a 1-D torch CUDA tensor (``.buffer``), not a Python list;
+* the element type is explicit: ``dtype`` in {float64 (default), float32,
+  int64}.  ``from_memory`` infers it (all-int -> int64, else float64,
+  float32 only when the source is float32);
+* ``.data`` is a host round trip (download on get, upload on set) kept for
+  compatibility with code that reads/assigns the reference's list;
+* relayout/assign run on the device (tl_copy).
+"""
+
+from __future__ import annotations
+
+import numbers
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _abi
+from .layout import TensorMeta, inverse_memory_index, memory_index, validate_layout, validate_shape, volume, zero_indices
+
+__all__ = ["DenseTensor", "tensors_equal", "as_dtype"]
+
+_NAMES = {
+    "float64": torch.float64, "f64": torch.float64, "double": torch.float64,
+    "float32": torch.float32, "f32": torch.float32, "float": torch.float32,
+    "int64": torch.int64, "i64": torch.int64, "int": torch.int64,
+}
+
+
+def as_dtype(dtype) -> torch.dtype:
+    if dtype is None:
+        return torch.float64
+    if isinstance(dtype, torch.dtype):
+        out = dtype
+    elif isinstance(dtype, str):
+        out = _NAMES[dtype]
+    else:
+        out = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+               np.dtype(np.int64): torch.int64}.get(np.dtype(dtype))
+    if out not in _abi.DTYPE_CODE:
+        raise TypeError(f"unsupported dtype {dtype!r}; use float64, float32 or int64")
+    return out
+
+
+def _default_device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1711_10912_b200 needs a CUDA (sm_100a) device; there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _infer_dtype(data) -> torch.dtype:
+    if isinstance(data, torch.Tensor):
+        if data.dtype in (torch.float32, torch.float64, torch.int64):
+            return data.dtype
+        return torch.float64 if data.is_floating_point() else torch.int64
+    if isinstance(data, np.ndarray):
+        if data.dtype == np.float32:
+            return torch.float32
+        if data.dtype.kind in "iub":
+            return torch.int64
+        return torch.float64
+    seq = list(data)
+    if seq and all(isinstance(x, numbers.Integral) and not isinstance(x, bool) for x in seq):
+        return torch.int64
+    return torch.float64
+
+
+class DenseTensor:
+    """Dense array with runtime order, extents, offsets and layout, stored
+    on the GPU in memory-index order."""
+
+    __slots__ = ("meta", "buffer")
+
+    def __init__(self, shape, offsets=None, layout=None, fill_value=0, dtype=None, device=None):
+        self.meta = TensorMeta(shape, offsets, layout)
+        dt = as_dtype(dtype)
+        dev = torch.device(device) if device is not None else _default_device()
+        self.buffer = torch.full((self.meta.size,), fill_value, dtype=dt, device=dev)
+
+    # -- construction -------------------------------------------------------------
+    @classmethod
+    def _wrap(cls, meta: TensorMeta, buffer: torch.Tensor) -> "DenseTensor":
+        t = cls.__new__(cls)
+        t.meta = meta
+        t.buffer = buffer
+        return t
+
+    @classmethod
+    def from_memory(cls, shape, data, offsets=None, layout=None, dtype=None, device=None) -> "DenseTensor":
+        """Copy a flat element sequence in memory order (tensor.py:48-59).
+
+        ``data`` may be a list/tuple, a numpy array or a torch tensor (host
+        or device; a pinned host tensor is copied asynchronously)."""
+        meta = TensorMeta(shape, offsets, layout)
+        dt = as_dtype(dtype) if dtype is not None else _infer_dtype(data)
+        dev = torch.device(device) if device is not None else _default_device()
+        if isinstance(data, torch.Tensor):
+            src = data.reshape(-1)
+            buf = torch.empty(src.numel(), dtype=dt, device=dev)
+            buf.copy_(src, non_blocking=src.is_pinned())
+        else:
+            arr = np.asarray(data if isinstance(data, np.ndarray) else list(data))
+            np_dt = {torch.float64: np.float64, torch.float32: np.float32, torch.int64: np.int64}[dt]
+            buf = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1), dtype=np_dt)).to(dev)
+        if buf.numel() != meta.size:
+            raise ValueError(f"data length {buf.numel()} does not match volume {meta.size}")
+        return cls._wrap(meta, buf)
+
+    # -- structure ----------------------------------------------------------------
+    @property
+    def shape(self):
+        return self.meta.shape
+
+    @property
+    def order(self) -> int:
+        return self.meta.order
+
+    @property
+    def layout(self):
+        return self.meta.layout
+
+    @property
+    def offsets(self):
+        return self.meta.offsets
+
+    @property
+    def strides(self):
+        return self.meta.strides
+
+    @property
+    def size(self) -> int:
+        return self.buffer.numel()
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.buffer.dtype
+
+    @property
+    def device(self) -> torch.device:
+        return self.buffer.device
+
+    def desc(self) -> _abi.TlDesc:
+        """The device layout descriptor (plays the MultiIterator's role)."""
+        return _abi.make_desc(self.shape, self.strides, _abi.DTYPE_CODE[self.dtype])
+
+    def ptr(self) -> int:
+        return self.buffer.data_ptr()
+
+    # -- host interchange ------------------------------------------------------------
+    @property
+    def data(self) -> list:
+        """Host copy of the buffer in memory-index order (a round trip)."""
+        return self.buffer.cpu().tolist()
+
+    @data.setter
+    def data(self, values) -> None:
+        src = values if isinstance(values, torch.Tensor) else torch.as_tensor(
+            np.asarray(list(values) if not isinstance(values, np.ndarray) else values))
+        src = src.reshape(-1)
+        if src.numel() != self.meta.size:
+            raise ValueError(f"data length {src.numel()} does not match volume {self.meta.size}")
+        self.buffer.copy_(src.to(self.dtype))
+
+    def numpy(self) -> np.ndarray:
+        return self.buffer.cpu().numpy()
+
+    def copy(self) -> "DenseTensor":
+        return DenseTensor._wrap(self.meta, self.buffer.clone())
+
+    # -- element access (host round trips; for tests and small tensors) -----------------
+    def _key(self, key) -> tuple:
+        key = (key,) if isinstance(key, numbers.Integral) else tuple(key)
+        if len(key) != self.order:
+            raise ValueError(f"expected {self.order} indices, got {len(key)}")
+        for r, (i, o, n) in enumerate(zip(key, self.offsets, self.shape)):
+            if not o <= i < o + n:
+                raise IndexError(f"index {i} out of bounds [{o}, {o + n}) in dimension {r + 1}")
+        return key
+
+    def __getitem__(self, key):
+        return self.buffer[memory_index(self.strides, self._key(key), self.offsets)].item()
+
+    def __setitem__(self, key, value):
+        self.buffer[memory_index(self.strides, self._key(key), self.offsets)] = value
+
+    def get_memory(self, j: int):
+        if not 0 <= j < self.size:
+            raise IndexError(f"memory index {j} out of range [0, {self.size})")
+        return self.buffer[j].item()
+
+    def set_memory(self, j: int, value) -> None:
+        if not 0 <= j < self.size:
+            raise IndexError(f"memory index {j} out of range [0, {self.size})")
+        self.buffer[j] = value
+
+    def item(self):
+        if self.size != 1:
+            raise ValueError(f"item() requires volume 1, got {self.size}")
+        return self.buffer[0].item()
+
+    # -- whole-tensor operations ---------------------------------------------------------
+    def fill(self, value) -> None:
+        self.buffer.fill_(value)
+
+    def relayout(self, new_layout) -> None:
+        """Physically reorder to ``new_layout`` keeping index -> value
+        (tensor.py:167-184), with the device copy kernel."""
+        new_layout = validate_layout(new_layout, self.order)
+        if new_layout == self.layout:
+            return
+        new_meta = TensorMeta(self.shape, self.offsets, new_layout)
+        out = torch.empty_like(self.buffer)
+        _copy(self.desc(), self.buffer, _abi.make_desc(self.shape, new_meta.strides, _abi.DTYPE_CODE[self.dtype]), out)
+        self.meta = new_meta
+        self.buffer = out
+
+    def assign(self, src) -> None:
+        """Copy src's values per zero-based multi-index (tensor.py:141-165)."""
+        if src is self:
+            return
+        if self.order == src.order:
+            meta = TensorMeta(src.shape, self.offsets, self.layout)
+        else:
+            meta = TensorMeta(src.shape, src.offsets, src.layout)
+        out = torch.empty(meta.size, dtype=src.dtype, device=src.device)
+        _copy(src.desc(), src.buffer, _abi.make_desc(meta.shape, meta.strides, _abi.DTYPE_CODE[src.dtype]), out)
+        self.meta = meta
+        self.buffer = out
+
+    def reshape(self, new_shape) -> None:
+        """Adopt a same-volume shape keeping the memory sequence (tensor.py:186-200)."""
+        new_shape = validate_shape(new_shape)
+        if volume(new_shape) != self.size:
+            raise ValueError(f"reshape to {new_shape} changes volume ({volume(new_shape)} != {self.size})")
+        self.meta = self.meta.with_shape(new_shape)
+
+    def to(self, dtype) -> "DenseTensor":
+        return DenseTensor._wrap(self.meta, self.buffer.to(as_dtype(dtype)))
+
+    # -- interchange -------------------------------------------------------------------
+    def to_dict(self) -> dict:
+        return {"shape": list(self.shape), "layout": list(self.layout), "offsets": list(self.offsets),
+                "data": self.data}
+
+    @classmethod
+    def from_dict(cls, obj: dict) -> "DenseTensor":
+        try:
+            shape, data = obj["shape"], obj["data"]
+            layout, offsets = obj.get("layout"), obj.get("offsets")
+        except (TypeError, KeyError) as exc:
+            raise ValueError(f"malformed tensor object: missing {exc}") from exc
+        return cls.from_memory(shape, data, offsets, layout)
+
+    def __eq__(self, other):
+        if not isinstance(other, DenseTensor):
+            return NotImplemented
+        return tensors_equal(self, other)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"DenseTensor(shape={self.shape}, offsets={self.offsets}, layout={self.layout}, dtype={self.dtype})"
+
+
+def _copy(adesc, abuf: torch.Tensor, cdesc, cbuf: torch.Tensor) -> None:
+    L = _abi.lib()
+    rc = L.tl_copy(adesc, abuf.data_ptr(), cdesc, cbuf.data_ptr(), _abi.stream_handle())
+    _abi.check(rc, "copy")
+
+
+def tensors_equal(a, b) -> bool:
+    """Equal order, shape and elements per zero-based multi-index; layout
+    and offsets are ignored (tensor.py:287-304)."""
+    if a.order != b.order or a.shape != b.shape:
+        return False
+    if a.layout == b.layout:
+        return bool(torch.equal(a.buffer, b.buffer.to(a.dtype)))
+    tmp = torch.empty_like(b.buffer)
+    _copy(b.desc(), b.buffer, _abi.make_desc(b.shape, a.strides, _abi.DTYPE_CODE[b.dtype]), tmp)
+    return bool(torch.equal(a.buffer, tmp.to(a.dtype)))

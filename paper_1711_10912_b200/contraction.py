@@ -68,7 +68,7 @@ def ttv(a, b, mode: int) -> DenseTensor:
     B = _vector(b, A.shape[mode - 1], "ttv vector")
     if _is_float(A.dtype) != _is_float(B.dtype):
         raise NotImplementedError("ttv: mixed integer and floating operands")
-    out = DenseTensor(A.shape[: mode - 1] + A.shape[mode:], dtype=A.dtype, device=A.device)
+    out = DenseTensor(A.shape[: mode - 1] + A.shape[mode:], dtype=A.dtype, device=A.device, fill_value=None)
     L = _abi.lib()
     rc = L.tl_ttv(A.desc(), A.ptr(), B.desc(), B.ptr(), out.desc(), out.ptr(), int(mode), _abi.stream_handle())
     _abi.check(rc, "ttv")
@@ -94,7 +94,7 @@ def ttm(a, bmat, mode: int) -> DenseTensor:
     if Bm.dtype != A.dtype:
         Bm = Bm.to(A.dtype)
     m = mode - 1
-    out = DenseTensor(A.shape[:m] + (Bm.shape[0],) + A.shape[m + 1:], dtype=A.dtype, device=A.device)
+    out = DenseTensor(A.shape[:m] + (Bm.shape[0],) + A.shape[m + 1:], dtype=A.dtype, device=A.device, fill_value=None)
     L = _abi.lib()
     rc = L.tl_ttm(A.desc(), A.ptr(), Bm.desc(), Bm.ptr(), out.desc(), out.ptr(), int(mode), _abi.stream_handle())
     _abi.check(rc, "ttm")
@@ -206,6 +206,6 @@ def times_matrices(a, matrices, modes) -> DenseTensor:
 
 
 def _first_order_copy(A: DenseTensor) -> DenseTensor:
-    out = DenseTensor(A.shape, dtype=A.dtype, device=A.device)
+    out = DenseTensor(A.shape, dtype=A.dtype, device=A.device, fill_value=None)
     _copy(A.desc(), A.buffer, out.desc(), out.buffer)
     return out

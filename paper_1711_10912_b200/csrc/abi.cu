@@ -21,6 +21,8 @@ int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
                      int m0, cudaStream_t st);
 int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                      int m0, cudaStream_t st);
+int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
+                       int m0, cudaStream_t st);
 size_t reduce_workspace_bytes();
 int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const void *b_ptr, void *result,
                    bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st);
@@ -198,10 +200,14 @@ int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void 
         return TL_EUNSUPPORTED;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    // GEMM-shaped float64 -> DMMA GETT; few rows J -> HBM-bound staged fold;
+    // anything else -> one-thread-per-output fold
     if (a->dtype == TL_F64) {
         int rc = ttm_dmma_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
         if (rc != TL_EUNSUPPORTED) return rc;
     }
+    int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+    if (rc != TL_EUNSUPPORTED) return rc;
     return ttm_simt_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
 }
 

@@ -172,38 +172,91 @@ as_acc(T v) {
 }
 
 // ------------------------------------------------------------ dot_rows
-template <class TA, class TB, int VEC>
+// Per-thread partial sums.  float32 operands: products are exact in
+// binary64, so one FMA per element (acc += a*b rounded once) into VEC
+// independent accumulators -- one FP64 op per element keeps the kernel
+// HBM-bound.  float64: TwoProd + TwoSum (double-double) per element.
+template <class TA> struct ThreadAcc {
+    DD dd[2];
+    __device__ void zero() { dd[0] = DD{0.0, 0.0}; dd[1] = DD{0.0, 0.0}; }
+    __device__ void add(int j, double x, double y) { dd_add_prod(dd[j & 1], x, y); }
+    __device__ DD total() const { return dd_merge(dd[0], dd[1]); }
+};
+template <> struct ThreadAcc<float> {
+    double s[4];
+    __device__ void zero() { s[0] = s[1] = s[2] = s[3] = 0.0; }
+    __device__ void add(int j, double x, double y) { s[j & 3] = fma(x, y, s[j & 3]); }
+    __device__ DD total() const {
+        DD r{s[0], 0.0};
+        two_sum_add(r, s[1]);
+        two_sum_add(r, s[2]);
+        two_sum_add(r, s[3]);
+        return r;
+    }
+};
+template <> struct ThreadAcc<int64_t> {
+    Acc64 a;
+    __device__ void zero() { a.v = 0; }
+    __device__ void add(int, int64_t x, int64_t y) { acc_prod(a, x, y); }
+    __device__ Acc64 total() const { return a; }
+};
+
+template <class T, int VEC> __device__ __forceinline__ void load_vec(const T *p, T (&x)[VEC]) {
+    if constexpr (VEC * sizeof(T) == 16) {
+        *(uint4 *)x = __ldcs((const uint4 *)p);
+    } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) x[j] = __ldcs(p + j);
+    }
+}
+
+template <class TA, class TB, int VEC, bool SAME>
 __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ ReduceParams P) {
     using Acc = typename RedAcc<TA>::type;
-    Acc acc;
-    acc_zero(acc);
+    ThreadAcc<TA> ta;
+    ta.zero();
     const TA *a = (const TA *)P.a;
     const TB *b = (const TB *)P.b;
     const int64_t L = P.row_len;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (P.n_rows == 1) {
-        // flat: 128-bit loads over the whole buffer
+        // flat: 128-bit streaming loads, 4 vectors in flight per thread
+        constexpr int U = 4;
         const int64_t nv = L / VEC;
-        for (int64_t v = tid; v < nv; v += nthreads) {
+        int64_t v = tid;
+        for (; v + (U - 1) * nthreads < nv; v += U * nthreads) {
+            TA xa[U][VEC];
+            TB xb[U][VEC];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                load_vec<TA, VEC>(a + (v + u * nthreads) * VEC, xa[u]);
+                if constexpr (!SAME) load_vec<TB, VEC>(b + (v + u * nthreads) * VEC, xb[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    if constexpr (SAME)
+                        ta.add(j, as_acc(xa[u][j]), as_acc(xa[u][j]));
+                    else
+                        ta.add(j, as_acc(xa[u][j]), as_acc(xb[u][j]));
+                }
+        }
+        for (; v < nv; v += nthreads) {
             TA xa[VEC];
             TB xb[VEC];
-            if constexpr (VEC * sizeof(TA) == 16) {
-                *(uint4 *)xa = __ldcs((const uint4 *)(a + v * VEC));
-            } else {
+            load_vec<TA, VEC>(a + v * VEC, xa);
+            if constexpr (!SAME) load_vec<TB, VEC>(b + v * VEC, xb);
 #pragma unroll
-                for (int j = 0; j < VEC; ++j) xa[j] = __ldcs(a + v * VEC + j);
+            for (int j = 0; j < VEC; ++j) {
+                if constexpr (SAME)
+                    ta.add(j, as_acc(xa[j]), as_acc(xa[j]));
+                else
+                    ta.add(j, as_acc(xa[j]), as_acc(xb[j]));
             }
-            if constexpr (VEC * sizeof(TB) == 16) {
-                *(uint4 *)xb = __ldcs((const uint4 *)(b + v * VEC));
-            } else {
-#pragma unroll
-                for (int j = 0; j < VEC; ++j) xb[j] = __ldcs(b + v * VEC + j);
-            }
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) acc_prod(acc, as_acc(xa[j]), as_acc(xb[j]));
         }
-        for (int64_t e = nv * VEC + tid; e < L; e += nthreads) acc_prod(acc, as_acc(a[e]), as_acc(b[e]));
+        for (int64_t e = nv * VEC + tid; e < L; e += nthreads) ta.add(0, as_acc(a[e]), as_acc(b[e]));
     } else {
         const int64_t total = P.n_rows * L;
         for (int64_t e = tid; e < total; e += nthreads) {
@@ -211,10 +264,10 @@ __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ R
             const int64_t c = e - r * L;
             const int64_t oa = P.rows_a.map((uint32_t)r) + c;
             const int64_t ob = P.rows_b.map((uint32_t)r) + c;
-            acc_prod(acc, as_acc(a[oa]), as_acc(b[ob]));
+            ta.add((int)c, as_acc(__ldcs(a + oa)), as_acc(__ldcs(b + ob)));
         }
     }
-    acc = block_reduce(acc);
+    Acc acc = block_reduce(ta.total());
     finish(P, acc);
 }
 
@@ -223,8 +276,8 @@ template <class TA, class TB>
 __global__ void __launch_bounds__(256) dot_tiled_kernel(const __grid_constant__ ReduceParams P) {
     using Acc = typename RedAcc<TA>::type;
     __shared__ TB tile[32][33];
-    Acc acc;
-    acc_zero(acc);
+    ThreadAcc<TA> ta;
+    ta.zero();
     const TA *a = (const TA *)P.a;
     const TB *b = (const TB *)P.b;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -245,11 +298,11 @@ __global__ void __launch_bounds__(256) dot_tiled_kernel(const __grid_constant__ 
         // a: coalesced along X (a's fastest dimension); b from the tile
         for (int yr = wid; yr < 32; yr += 8) {
             const int64_t x = x0 + lane, y = y0 + yr;
-            if (x < P.nX && y < P.nY) acc_prod(acc, as_acc(__ldcs(a + ra + x + y * P.a_sY)), as_acc(tile[lane][yr]));
+            if (x < P.nX && y < P.nY) ta.add(yr, as_acc(__ldcs(a + ra + x + y * P.a_sY)), as_acc(tile[lane][yr]));
         }
         __syncthreads();
     }
-    acc = block_reduce(acc);
+    Acc acc = block_reduce(ta.total());
     finish(P, acc);
 }
 
@@ -316,29 +369,29 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         }
         build_map(DigitList{{P.n_rows, row_len}}, P.rows_a);
         if (!build_map(rb, P.rows_b)) return TL_EUNSUPPORTED;
-        const int64_t work = (P.n_rows == 1) ? N / 4 : N;
-        int64_t grid = std::min<int64_t>((int64_t)di.num_sms * 8, (work + threads - 1) / threads);
+        // persistent grid: 4 CTAs per SM, each thread keeps 4 x 16 B in flight
+        const int64_t work = (P.n_rows == 1) ? N / 16 : N / 4;
+        int64_t grid = std::min<int64_t>((int64_t)di.num_sms * 4, (work + threads - 1) / threads);
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, kMaxPartials));
         const uintptr_t pa = (uintptr_t)P.a, pb = (uintptr_t)P.b;
+        const bool same = (P.a == P.b) && (a.dtype == b.dtype) && P.n_rows == 1;
+        const bool al = (pa % 16 == 0 && pb % 16 == 0);
+        const unsigned G = (unsigned)grid;
         if (a.dtype == TL_F32 && b.dtype == TL_F32) {
-            if (pa % 16 == 0 && pb % 16 == 0)
-                dot_rows_kernel<float, float, 4><<<(unsigned)grid, threads, 0, st>>>(P);
-            else
-                dot_rows_kernel<float, float, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+            if (same && al) dot_rows_kernel<float, float, 4, true><<<G, threads, 0, st>>>(P);
+            else if (al) dot_rows_kernel<float, float, 4, false><<<G, threads, 0, st>>>(P);
+            else dot_rows_kernel<float, float, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F64 && b.dtype == TL_F64) {
-            if (pa % 16 == 0 && pb % 16 == 0)
-                dot_rows_kernel<double, double, 2><<<(unsigned)grid, threads, 0, st>>>(P);
-            else
-                dot_rows_kernel<double, double, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+            if (same && al) dot_rows_kernel<double, double, 2, true><<<G, threads, 0, st>>>(P);
+            else if (al) dot_rows_kernel<double, double, 2, false><<<G, threads, 0, st>>>(P);
+            else dot_rows_kernel<double, double, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F32 && b.dtype == TL_F64) {
-            dot_rows_kernel<float, double, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+            dot_rows_kernel<float, double, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F64 && b.dtype == TL_F32) {
-            dot_rows_kernel<double, float, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+            dot_rows_kernel<double, float, 1, false><<<G, threads, 0, st>>>(P);
         } else {
-            if (pa % 16 == 0 && pb % 16 == 0)
-                dot_rows_kernel<int64_t, int64_t, 2><<<(unsigned)grid, threads, 0, st>>>(P);
-            else
-                dot_rows_kernel<int64_t, int64_t, 1><<<(unsigned)grid, threads, 0, st>>>(P);
+            if (al) dot_rows_kernel<int64_t, int64_t, 2, false><<<G, threads, 0, st>>>(P);
+            else dot_rows_kernel<int64_t, int64_t, 1, false><<<G, threads, 0, st>>>(P);
         }
         e = cudaGetLastError();
     } else {

@@ -1,9 +1,362 @@
-// ttm_dmma.cu -- float64 ttm as a GETT on FP64 DMMA tensor cores (placeholder
-// until the tiled kernel lands; tl_ttm falls back to the exact SIMT fold).
+// ttm_dmma.cu -- float64 ttm (contraction.py:200-298) as a GETT on the FP64
+// tensor cores (mma.sync f64 -> SASS DMMA.8x8x4; tcgen05 has no f64 kind).
+//
+// For dense A of any permutation layout (plan.h: A[O][K][I]) the product is
+//     C[j, f] = sum_k B[j, k] * A'[k, f],    f = o*I + i  (free positions)
+// i.e. one GEMM with M = J (rows of B), N = O*I, K = n_mode, where the
+// operand A' and the first-order output are addressed through tables:
+//     A'(k, f) = A + aoff[f] + k*I,     C(j, f) = C + coff[f] + j*jstride.
+// The N dimension of a CTA tile is BN consecutive positions of a host-chosen
+// ordering sigma of the free digits (possibly splitting digits), which makes
+// the A' loads and the C stores coalesce for every layout/mode:
+//   * output contiguous along j (mode 1): sigma = A's order,
+//   * A contiguous along k (I == 1):       sigma = C's order,
+//   * otherwise a 2-D box: 8 positions along A's fastest free digit x 16
+//     along the output's fastest free digit (64-byte load runs; each CTA
+//     writes whole 32-byte sectors of C).
+// CTA tile 128 (J) x 128 (free) x 32 (k), FP64 m16n8k4 MMAs, 3-stage
+// cp.async pipeline, operands in padded shared memory (pitch = 4 mod 16
+// doubles: conflict-free fragment loads), fragments double-buffered in
+// registers, epilogue writes straight to first-order C.  Two warp layouts:
+// 8 warps of 64x32 (Cfg8) or 16 warps of 32x32 (Cfg16, <= 128 registers,
+// twice the warps to hide the DMMA issue latency).
+//
+// Numerics: DMMA accumulates k in order with fused multiply-adds (measured
+// on B200: DMMA.8x8x4 == 4 sequential FMAs), so results differ from the
+// reference's separately rounded fold by at most ~K ulps of sum_k |A||B|;
+// parity is checked at 1e-12 of that bound (tests/).
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "plan.h"
 #include "tl_common.cuh"
 
 namespace tl {
-int ttm_dmma_enqueue(const tl_desc &, const void *, const tl_desc &, const void *, void *, int, cudaStream_t) {
-    return TL_EUNSUPPORTED;
+
+namespace gett {
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int NST = 3;
+constexpr int LDW = BN + 4;  // pitch of [k][n] / [k][m] tiles (doubles)
+constexpr int LDK = BK + 4;  // pitch of [n][k] / [m][k] tiles (doubles)
+constexpr int A_TILE = BK * LDW > BN * LDK ? BK * LDW : BN * LDK;  // doubles
+constexpr int B_TILE = BK * LDW > BM * LDK ? BK * LDW : BM * LDK;
+constexpr size_t SMEM = (size_t)NST * (A_TILE + B_TILE) * 8 + (size_t)BN * 16;
+}  // namespace gett
+
+// warp layout: WM x WN warps, each TM m16 tiles x TN n8 tiles
+template <int WM_, int WN_, int TM_, int TN_> struct GettCfg {
+    static constexpr int WM = WM_, WN = WN_, TM = TM_, TN = TN_;
+    static constexpr int THREADS = 32 * WM * WN;
+    static_assert(WM * TM * 16 == gett::BM && WN * TN * 8 == gett::BN, "tile mismatch");
+};
+using Cfg8 = GettCfg<2, 4, 4, 4>;
+using Cfg16 = GettCfg<4, 4, 2, 4>;
+
+struct TtmParams {
+    const double *a;
+    const double *b;
+    double *c;
+    int64_t J, K, I, F;
+    int64_t jstride;
+    int64_t bs0, bs1;
+    int32_t mtiles;
+    int32_t nd;  // sigma digits (fastest first)
+    FastDiv dig[TL_MAX_DIGITS + 1];
+    int64_t dig_a[TL_MAX_DIGITS + 1];
+    int64_t dig_c[TL_MAX_DIGITS + 1];
+};
+
+__device__ __forceinline__ void cp_async8_zfill(void *smem_dst, const void *gmem_src, bool valid) {
+    const int n = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(n));
 }
+
+__device__ __forceinline__ void mma_16x8x4(double (&d)[4], const double (&a)[2], double b) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+                 : "d"(a[0]), "d"(a[1]), "d"(b));
+}
+
+template <class CFG, bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_constant__ TtmParams P) {
+    using namespace gett;
+    constexpr int THREADS = CFG::THREADS, TM = CFG::TM, TN = CFG::TN, WN = CFG::WN;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *As = (double *)smem_raw;                 // NST x A_TILE
+    double *Bs = As + NST * A_TILE;                  // NST x B_TILE
+    int64_t *aoff = (int64_t *)(Bs + NST * B_TILE);  // BN
+    int64_t *coff = aoff + BN;                       // BN  (-1: masked column)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp / WN;
+    const int wn = warp % WN;
+    const int mt = blockIdx.x % P.mtiles;
+    const int64_t nt = blockIdx.x / P.mtiles;
+    const int64_t m0 = (int64_t)mt * BM;
+
+    // column tables for this N tile (sigma-ordered free positions)
+    if (tid < BN) {
+        const int64_t q = nt * BN + tid;
+        int64_t ao = 0, co = -1;
+        if (q < P.F) {
+            uint32_t x = (uint32_t)q;
+            co = 0;
+            for (int d = 0; d < P.nd; ++d) {
+                uint32_t qq, r;
+                if (d == P.nd - 1) {
+                    r = x;
+                    qq = 0;
+                } else {
+                    P.dig[d].divmod(x, qq, r);
+                }
+                ao += (int64_t)r * P.dig_a[d];
+                co += (int64_t)r * P.dig_c[d];
+                x = qq;
+            }
+        }
+        aoff[tid] = ao;
+        coff[tid] = co;
+    }
+    __syncthreads();
+
+    const int64_t K = P.K, I = P.I;
+    const int KT = (int)((K + BK - 1) / BK);
+
+    // Per-thread load assignment, fixed for the whole tile.  K-major
+    // operands: lanes walk k (fixed k column per thread); otherwise lanes
+    // walk n/m (fixed column, k rows).  Base pointers are formed once.
+    constexpr int LPT = (BK * BN) / THREADS;
+    const int a_kk0 = A_KMAJOR ? (tid & (BK - 1)) : (tid / BN);
+    const int a_nn0 = A_KMAJOR ? (tid / BK) : (tid & (BN - 1));
+    const int b_kk0 = B_KMAJOR ? (tid & (BK - 1)) : (tid / BM);
+    const int b_mm0 = B_KMAJOR ? (tid / BK) : (tid & (BM - 1));
+    const double *a_base_fixed = P.a + aoff[a_nn0];
+    const bool a_col_ok = coff[a_nn0] >= 0;
+    const double *b_base_fixed = P.b + (m0 + b_mm0) * P.bs0;
+    const bool b_row_ok = (m0 + b_mm0) < P.J;
+
+    auto load_stage = [&](int stage, int kt) {
+        const int64_t k0 = (int64_t)kt * BK;
+        double *as = As + stage * A_TILE;
+        double *bs = Bs + stage * B_TILE;
+#pragma unroll
+        for (int s = 0; s < LPT; ++s) {
+            if constexpr (A_KMAJOR) {
+                const int nn = a_nn0 + s * (THREADS / BK);
+                const int64_t k = k0 + a_kk0;
+                const bool ok = (k < K) && (coff[nn] >= 0);
+                cp_async8_zfill(as + nn * LDK + a_kk0, P.a + (ok ? aoff[nn] + k : 0), ok);
+            } else {
+                const int kk = a_kk0 + s * (THREADS / BN);
+                const int64_t k = k0 + kk;
+                const bool ok = a_col_ok && (k < K);
+                cp_async8_zfill(as + kk * LDW + a_nn0, ok ? a_base_fixed + k * I : P.a, ok);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < LPT; ++s) {
+            if constexpr (B_KMAJOR) {
+                const int mm = b_mm0 + s * (THREADS / BK);
+                const int64_t k = k0 + b_kk0, j = m0 + mm;
+                const bool ok = (k < K) && (j < P.J);
+                cp_async8_zfill(bs + mm * LDK + b_kk0, P.b + (ok ? j * P.bs0 + k : 0), ok);
+            } else {
+                const int kk = b_kk0 + s * (THREADS / BM);
+                const int64_t k = k0 + kk;
+                const bool ok = b_row_ok && (k < K);
+                cp_async8_zfill(bs + kk * LDW + b_mm0, ok ? b_base_fixed + k * P.bs1 : P.b, ok);
+            }
+        }
+    };
+
+    double acc[TM][TN][4];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) {
+        if (s < KT) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<NST - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + NST - 1;
+            if (nk < KT) load_stage(nk % NST, nk);
+            cp_async_commit();
+        }
+        const double *as = As + (kt % NST) * A_TILE;
+        const double *bs = Bs + (kt % NST) * B_TILE;
+        // fragments double-buffered in registers: step k4+1 is loaded from
+        // shared memory while step k4's MMAs issue
+        double af[2][TM][2], bf[2][TN];
+        auto load_frags = [&](int buf, int k4) {
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                const int m = wm * (16 * TM) + i * 16 + g;
+                if constexpr (B_KMAJOR) {
+                    af[buf][i][0] = bs[m * LDK + k4 + t];
+                    af[buf][i][1] = bs[(m + 8) * LDK + k4 + t];
+                } else {
+                    af[buf][i][0] = bs[(k4 + t) * LDW + m];
+                    af[buf][i][1] = bs[(k4 + t) * LDW + m + 8];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int n = wn * (8 * TN) + j * 8 + g;
+                bf[buf][j] = A_KMAJOR ? as[n * LDK + k4 + t] : as[(k4 + t) * LDW + n];
+            }
+        };
+        load_frags(0, 0);
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            const int cur = (k4 / 4) & 1;
+            if (k4 + 4 < BK) load_frags(cur ^ 1, k4 + 4);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) mma_16x8x4(acc[i][j], af[cur][i], bf[cur][j]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // epilogue: fragments -> first-order C
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j = m0 + wm * (16 * TM) + i * 16 + g + 8 * h;
+            if (j >= P.J) continue;
+            const int64_t jo = j * P.jstride;
+#pragma unroll
+            for (int jj = 0; jj < TN; ++jj) {
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int n = wn * (8 * TN) + jj * 8 + 2 * t + v;
+                    const int64_t co = coff[n];
+                    if (co >= 0) P.c[co + jo] = acc[i][jj][2 * h + v];
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ planning
+struct Digit {
+    int64_t ext, as, cs;  // extent, A stride, C stride
+};
+
+static int gett_variant() {
+    static int v = [] {
+        const char *e = getenv("TL_GETT_WARPS");
+        return (e && atoi(e) == 8) ? 8 : 16;
+    }();
+    return v;
+}
+
+int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
+                     cudaStream_t st) {
+    using namespace gett;
+    const int64_t J = bm.extent[0];
+    Canon cn;
+    if (!canon_contraction(a, m0, J, cn)) {
+        set_error("ttm: operand A is not a dense permutation layout (materialise views first)");
+        return TL_EUNSUPPORTED;
+    }
+    const int64_t F = cn.O * cn.I;
+    // GEMM-shaped only: small J or K is HBM-bound and goes to the staged kernel
+    if (J < 32 || cn.K < 16 || F < 64 || F > 0xffffffffll) return TL_EUNSUPPORTED;
+
+    // free digits in A order with A strides
+    std::vector<Digit> dg;
+    {
+        int64_t run = 1;
+        for (auto &d : cn.inner) {
+            dg.push_back({d.first, run, d.second});
+            run *= d.first;
+        }
+        run = cn.K * cn.I;
+        for (auto &d : cn.outer) {
+            dg.push_back({d.first, run, d.second});
+            run *= d.first;
+        }
+    }
+    const bool a_kmajor = (cn.I == 1);
+    std::vector<Digit> sigma;
+    if (cn.jstride == 1 || dg.empty()) {
+        sigma = dg;  // output contiguous along j: keep A's order
+    } else if (a_kmajor) {
+        sigma = dg;
+        std::stable_sort(sigma.begin(), sigma.end(), [](const Digit &x, const Digit &y) { return x.cs < y.cs; });
+    } else {
+        // fastest free digit of A (inner, stride 1) vs of C
+        size_t ic = 0;
+        for (size_t d = 1; d < dg.size(); ++d)
+            if (dg[d].cs < dg[ic].cs) ic = d;
+        if (ic == 0) {
+            sigma = dg;
+        } else {
+            // 2-D box: 8 along A's fastest digit (64-byte load runs) x 16
+            // along C's fastest digit (whole sectors of C per CTA)
+            const Digit dc = dg[ic], da = dg[0];
+            const int64_t alo = (da.ext % 8 == 0 && da.ext > 8) ? 8 : da.ext;
+            const int64_t clo = (dc.ext % 16 == 0 && dc.ext > 16) ? 16 : dc.ext;
+            sigma.push_back({alo, da.as, da.cs});
+            sigma.push_back({clo, dc.as, dc.cs});
+            if (alo < da.ext) sigma.push_back({da.ext / alo, da.as * alo, da.cs * alo});
+            if (clo < dc.ext) sigma.push_back({dc.ext / clo, dc.as * clo, dc.cs * clo});
+            for (size_t d = 1; d < dg.size(); ++d)
+                if (d != ic) sigma.push_back(dg[d]);
+        }
+    }
+    if (sigma.size() > TL_MAX_DIGITS + 1) return TL_EUNSUPPORTED;
+
+    TtmParams P{};
+    P.a = (const double *)a_ptr + a.offset;
+    P.b = (const double *)b_ptr + bm.offset;
+    P.c = (double *)c_ptr;
+    P.J = J;
+    P.K = cn.K;
+    P.I = cn.I;
+    P.F = F;
+    P.jstride = cn.jstride;
+    P.bs0 = bm.stride[0];
+    P.bs1 = bm.stride[1];
+    P.mtiles = (int32_t)((J + BM - 1) / BM);
+    if (sigma.empty()) sigma.push_back({1, 0, 0});
+    P.nd = (int32_t)sigma.size();
+    for (size_t d = 0; d < sigma.size(); ++d) {
+        P.dig[d].init((uint32_t)sigma[d].ext);
+        P.dig_a[d] = sigma[d].as;
+        P.dig_c[d] = sigma[d].cs;
+    }
+    const int64_t ntiles = (F + BN - 1) / BN;
+    const int64_t grid = ntiles * P.mtiles;
+    if (grid > 0x7fffffffll) return TL_EUNSUPPORTED;
+    const bool b_kmajor = (bm.stride[1] == 1 && bm.extent[1] > 1);
+    auto go = [&](auto kern, int threads) -> int {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        if (e != cudaSuccess) return cuda_status(e, "ttm smem attribute");
+        kern<<<(unsigned)grid, threads, SMEM, st>>>(P);
+        return cuda_status(cudaGetLastError(), "ttm dmma launch");
+    };
+    if (gett_variant() == 8) {
+        constexpr int T = Cfg8::THREADS;
+        if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg8, true, true>, T) : go(ttm_dmma_kernel<Cfg8, true, false>, T);
+        return b_kmajor ? go(ttm_dmma_kernel<Cfg8, false, true>, T) : go(ttm_dmma_kernel<Cfg8, false, false>, T);
+    }
+    constexpr int T = Cfg16::THREADS;
+    if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg16, true, true>, T) : go(ttm_dmma_kernel<Cfg16, true, false>, T);
+    return b_kmajor ? go(ttm_dmma_kernel<Cfg16, false, true>, T) : go(ttm_dmma_kernel<Cfg16, false, false>, T);
+}
+
 }  // namespace tl

@@ -1,10 +1,20 @@
-// ttm_simt.cu -- exact-fold ttm (contraction.py:200-298) for int64 operands
-// and for shapes the DMMA GETT does not tile (tiny J or K).
+// ttm_simt.cu -- ttm (contraction.py:200-298) for shapes that are not
+// GEMM-shaped: few output rows J (HBM-bound, e.g. config 5's 16 x 33
+// matrix), int64 and float32 operands.
 //
-// One thread per output C(o, j, i) folds k in order from 0 with separately
-// rounded binary64 products and sums -- the reference's arithmetic, so the
-// result is bit-identical.  The matrix B is read through L1 (lanes of a warp
-// share j or k), A is coalesced along the inner block when I >= 32.
+// ttm_staged: a persistent CTA streams tiles of R consecutive [K][I] blocks
+// of A (one contiguous byte range) into shared memory with a 1-D TMA bulk
+// copy, keeps B in shared memory, and each thread folds one (row, i) for up
+// to 16 j's at a time in registers (B reads are warp broadcasts).  The
+// output tile, contiguous in first-order C when the layout allows, is
+// staged in shared memory and written with coalesced stores.  Arithmetic:
+// int64 exact; float32 widened to binary64 where every product is exact, so
+// fma == the reference's mul-then-add and results are bit-identical;
+// float64 uses fma (the DMMA semantics) within the stated 1e-12 tolerance.
+//
+// ttm_simt: one thread per output, the reference's fold (fallback).
+#include <algorithm>
+
 #include "plan.h"
 #include "tl_common.cuh"
 
@@ -19,6 +29,10 @@ struct TtmSimtParams {
     int64_t jstride;   // output stride of j
     int32_t ident;
     DigitMap in_map, out_map;
+    // staged plan
+    int32_t R;
+    int64_t ntiles;
+    FastDiv I_div;
 };
 
 template <class T, class TC>
@@ -44,15 +58,221 @@ __global__ void __launch_bounds__(256) ttm_simt_kernel(const __grid_constant__ T
     ((TC *)P.c)[off] = narrow<TC>(acc);
 }
 
-int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
-                     int m0, cudaStream_t st) {
+// ------------------------------------------------------------ staged (small J)
+constexpr int kTtmStages = 4;
+constexpr int kJB = 16;
+
+template <class T> __device__ __forceinline__ typename AccOf<T>::type mac(typename AccOf<T>::type acc, T a, typename AccOf<T>::type b);
+template <> __device__ __forceinline__ double mac<double>(double acc, double a, double b) { return fma(a, b, acc); }
+template <> __device__ __forceinline__ double mac<float>(double acc, float a, double b) { return fma((double)a, b, acc); }
+template <> __device__ __forceinline__ int64_t mac<int64_t>(int64_t acc, int64_t a, int64_t b) { return fold_step(acc, a, b); }
+
+// Shared-memory image of B.  SIMT: Bt[k][jpad] (j contiguous, jpad = J
+// rounded up to 16, zero padded) so the 16 b(j, k) of one k are 8 vector
+// broadcast loads.  DMMA: Bm[m][ldb] with ldb = 4 (mod 16) doubles
+// (conflict-free A-fragment loads), zero padded in m and k.
+__host__ __device__ __forceinline__ int64_t ttm_jpad(int64_t J) { return (J + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int64_t ttm_ldb(int64_t K) {
+    int64_t l = (K + 3) / 4 * 4;
+    while (l % 16 != 4) l += 4;
+    return l;
+}
+
+template <class T, bool DMMA> struct StagedLayout {
+    size_t bbytes;
+    __host__ __device__ StagedLayout(int64_t J, int64_t K) {
+        const size_t n = DMMA ? (size_t)ttm_jpad(J) * ttm_ldb(K) : (size_t)K * ttm_jpad(J);
+        bbytes = (n * sizeof(typename AccOf<T>::type) + 15) & ~(size_t)15;
+    }
+};
+
+__device__ __forceinline__ void mma_16x8x4_s(double (&d)[4], double a0, double a1, double b) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+                 : "d"(a0), "d"(a1), "d"(b));
+}
+
+template <class T, bool DMMA>
+__global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__ TtmSimtParams P) {
+    using Acc = typename AccOf<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[kTtmStages];
+    const int64_t K = P.K, I = P.I, J = P.J;
+    const int64_t KI = K * I;
+    const int64_t jpad = ttm_jpad(J);
+    // layout: B image | stages (R*K*I elements) | output tile (R*J*I)
+    Acc *bsm = (Acc *)smem_raw;
+    const size_t bbytes = StagedLayout<T, DMMA>(J, K).bbytes;
+    unsigned char *stages = smem_raw + bbytes;
+    const size_t stage_bytes = ((size_t)P.R * KI * sizeof(T) + 15) & ~(size_t)15;
+    T *outs = (T *)(stages + kTtmStages * stage_bytes);
+
+    if constexpr (DMMA) {
+        const int64_t ldb = ttm_ldb(K);
+        for (int64_t e = threadIdx.x; e < jpad * ldb; e += blockDim.x) {
+            const int64_t j = e / ldb, k = e - j * ldb;
+            bsm[e] = (j < J && k < K) ? (Acc)((const T *)P.bm)[j * P.bs0 + k * P.bs1] : Acc(0);
+        }
+    } else {
+        for (int64_t e = threadIdx.x; e < K * jpad; e += blockDim.x) {
+            const int64_t k = e / jpad, j = e - k * jpad;
+            bsm[e] = (j < J) ? (Acc)((const T *)P.bm)[j * P.bs0 + k * P.bs1] : Acc(0);
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTtmStages; ++s) mbar_init(&full_bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    auto issue = [&](int64_t q) {
+        const int s = (int)(q % kTtmStages);
+        const int64_t tile = (int64_t)blockIdx.x + q * gridDim.x;
+        const int64_t o0 = tile * P.R;
+        const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
+        const uint32_t bytes = (uint32_t)(rows * KI * (int64_t)sizeof(T));
+        const uint32_t b16 = bytes & ~15u;
+        unsigned char *dst = stages + s * stage_bytes;
+        const unsigned char *src = (const unsigned char *)((const T *)P.a + o0 * KI);
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], b16);
+            if (b16) bulk_g2s(dst, src, b16, &full_bar[s]);
+        }
+        const uint32_t tail = (bytes - b16) / (uint32_t)sizeof(T);
+        if (threadIdx.x < tail) cp_async<sizeof(T)>(dst + b16 + threadIdx.x * sizeof(T), src + b16 + threadIdx.x * sizeof(T));
+    };
+#pragma unroll
+    for (int q = 0; q < kTtmStages - 1; ++q) {
+        if (q < my_tiles) issue(q);
+        cp_async_commit();
+    }
+
+    const uint32_t slots = (uint32_t)(P.R * I);
+    for (int64_t q = 0; q < my_tiles; ++q) {
+        cp_async_wait<kTtmStages - 2>();
+        mbar_wait_parity(&full_bar[q % kTtmStages], (uint32_t)((q / kTtmStages) & 1));
+        __syncthreads();
+        if (q + kTtmStages - 1 < my_tiles) issue(q + kTtmStages - 1);
+        cp_async_commit();
+        const T *st = (const T *)(stages + (q % kTtmStages) * stage_bytes);
+        const int64_t tile = (int64_t)blockIdx.x + q * gridDim.x;
+        const int64_t o0 = tile * P.R;
+        const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
+        auto put = [&](uint32_t r, uint32_t i, int64_t j, Acc v) {
+            if (r >= rows || j >= J) return;
+            if (P.ident) {
+                outs[((size_t)r * J + j) * I + i] = narrow<T>(v);
+            } else {
+                ((T *)P.c)[P.out_map.map((uint32_t)(o0 + r)) + j * P.jstride + P.in_map.map(i)] = narrow<T>(v);
+            }
+        };
+        if constexpr (DMMA) {
+            // warp w takes groups of 32 positions (4 n8 tiles); all J rows
+            // (jpad/16 m16 tiles); k in steps of 4 with zero padding
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+            const int g = lane >> 2, t = lane & 3;
+            const int64_t ldb = ttm_ldb(K);
+            const int mtiles = (int)(jpad / 16);
+            for (uint32_t p0 = warp * 32; p0 < slots; p0 += nw * 32) {
+                // this lane's B-fragment column positions (n = g) for the 4 tiles
+                int64_t base[4];
+                bool okp[4];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    uint32_t r, i;
+                    const uint32_t pos = p0 + nt * 8 + g;
+                    P.I_div.divmod(pos, r, i);
+                    okp[nt] = pos < slots && r < rows;
+                    base[nt] = (int64_t)r * KI + i;
+                }
+                for (int mt = 0; mt < mtiles; mt += 4) {
+                    double acc[4][4][4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+                    for (int64_t k4 = 0; k4 < K; k4 += 4) {
+                        const int64_t k = k4 + t;
+                        double bf[4];
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt)
+                            bf[nt] = (okp[nt] && k < K) ? (double)st[base[nt] + k * I] : 0.0;
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm) {
+                            if (mt + mm >= mtiles) break;
+                            const double *brow = (const double *)bsm + ((mt + mm) * 16 + g) * ldb + k4 + t;
+                            const double a0 = brow[0], a1 = brow[8 * ldb];
+#pragma unroll
+                            for (int nt = 0; nt < 4; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
+                        }
+                    }
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        if (mt + mm >= mtiles) break;
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                const uint32_t pos = p0 + nt * 8 + 2 * t + (v & 1);
+                                const int64_t j = (mt + mm) * 16 + g + 8 * (v >> 1);
+                                if (pos < slots) {
+                                    uint32_t r, i;
+                                    P.I_div.divmod(pos, r, i);
+                                    put(r, i, j, (Acc)acc[mm][nt][v]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        } else {
+            for (uint32_t slot = threadIdx.x; slot < slots; slot += blockDim.x) {
+                uint32_t r, i;
+                P.I_div.divmod(slot, r, i);
+                if (r >= rows) continue;
+                const T *arow = st + (size_t)r * KI + i;
+                for (int64_t j0 = 0; j0 < J; j0 += kJB) {
+                    Acc acc[kJB];
+#pragma unroll
+                    for (int jj = 0; jj < kJB; ++jj) acc[jj] = Acc(0);
+                    for (int64_t k = 0; k < K; ++k) {
+                        const T av = arow[k * I];
+                        // 16 consecutive b(j, k) of this k: vector broadcast loads
+                        const uint4 *bk = (const uint4 *)(bsm + k * jpad + j0);
+                        Acc bv[kJB];
+#pragma unroll
+                        for (int q4 = 0; q4 < kJB * (int)sizeof(Acc) / 16; ++q4) ((uint4 *)bv)[q4] = bk[q4];
+#pragma unroll
+                        for (int jj = 0; jj < kJB; ++jj) acc[jj] = mac<T>(acc[jj], av, bv[jj]);
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < kJB; ++jj) put(r, i, j0 + jj, acc[jj]);
+                }
+            }
+        }
+        if (P.ident) {
+            __syncthreads();
+            // the tile's outputs are one contiguous range of first-order C
+            T *dst = (T *)P.c + o0 * J * I;
+            const int64_t n = rows * J * I;
+            for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = outs[e];
+        }
+    }
+    cp_async_wait<0>();
+}
+
+static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
+                         int m0, TtmSimtParams &P) {
     const int64_t J = bm.extent[0];
     Canon cn;
     if (!canon_contraction(a, m0, J, cn)) {
         set_error("ttm: operand A is not a dense permutation layout (materialise views first)");
-        return TL_EUNSUPPORTED;
+        return false;
     }
-    TtmSimtParams P{};
     const size_t s = dtype_size(a.dtype);
     P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)s;
     P.bm = (const unsigned char *)b_ptr + bm.offset * (int64_t)dtype_size(bm.dtype);
@@ -65,7 +285,57 @@ int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     P.bs1 = bm.stride[1];
     P.jstride = cn.jstride;
     P.ident = cn.ident ? 1 : 0;
-    if (!build_map(cn.inner, P.in_map) || !build_map(cn.outer, P.out_map)) return TL_EUNSUPPORTED;
+    if (!build_map(cn.inner, P.in_map) || !build_map(cn.outer, P.out_map)) {
+        set_error("ttm: extent exceeds 32-bit digit range");
+        return false;
+    }
+    return true;
+}
+
+int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
+                       int m0, cudaStream_t st) {
+    TtmSimtParams P{};
+    if (!build_params(a, a_ptr, bm, b_ptr, c_ptr, m0, P)) return TL_EUNSUPPORTED;
+    const int64_t s = (int64_t)dtype_size(a.dtype);
+    const int64_t KI = P.K * P.I;
+    const uintptr_t base = (uintptr_t)P.a;
+    if (P.O * P.I == 0) return TL_OK;
+    if (P.I > 256 || KI * s > 32 * 1024 || P.J * P.K * 8 > 48 * 1024 || base % 16 != 0 || P.O > 0xffffffffll)
+        return TL_EUNSUPPORTED;
+    const int64_t stage_target = 20 * 1024;
+    int64_t R = std::max<int64_t>(1, std::min<int64_t>(256 / P.I, stage_target / (KI * s)));
+    // keep every tile's start 16-byte aligned for the bulk copy
+    while (R > 1 && (R * KI * s) % 16 != 0) --R;
+    if ((R * KI * s) % 16 != 0 && P.O > R) return TL_EUNSUPPORTED;
+    P.R = (int32_t)R;
+    P.ntiles = (P.O + R - 1) / R;
+    P.I_div.init((uint32_t)P.I);
+    const bool dmma = (a.dtype == TL_F64);  // FP64 tensor cores for float64
+    const int threads = (int)std::min<int64_t>(256, std::max<int64_t>(32, ((R * P.I + 31) / 32) * 32));
+    const size_t bbytes = dmma ? StagedLayout<double, true>(P.J, P.K).bbytes
+                               : (a.dtype == TL_F32 ? StagedLayout<float, false>(P.J, P.K).bbytes
+                                                    : StagedLayout<int64_t, false>(P.J, P.K).bbytes);
+    const size_t stage_bytes = ((size_t)R * KI * s + 15) & ~(size_t)15;
+    const size_t smem = bbytes + kTtmStages * stage_bytes + (size_t)R * P.J * P.I * s;
+    if (smem > 200 * 1024) return TL_EUNSUPPORTED;
+    const DeviceInfo &di = device_info();
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (228 * 1024) / (int64_t)(smem + 2048)));
+    const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * per_sm);
+    auto go = [&](auto kern) -> int {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_status(e, "ttm staged smem");
+        kern<<<(unsigned)grid, threads, smem, st>>>(P);
+        return cuda_status(cudaGetLastError(), "ttm staged launch");
+    };
+    if (dmma) return go(ttm_staged_kernel<double, true>);
+    if (a.dtype == TL_F32) return go(ttm_staged_kernel<float, false>);
+    return go(ttm_staged_kernel<int64_t, false>);
+}
+
+int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
+                     int m0, cudaStream_t st) {
+    TtmSimtParams P{};
+    if (!build_params(a, a_ptr, bm, b_ptr, c_ptr, m0, P)) return TL_EUNSUPPORTED;
     const int64_t total = P.O * P.J * P.I;
     if (total == 0) return TL_OK;
     const int threads = 256;

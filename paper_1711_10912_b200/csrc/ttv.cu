@@ -158,6 +158,27 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
 constexpr int kStages = 3;
 constexpr int kMaxOpt = 4;
 
+// Contiguous-chunk mode (one k-slab, unpadded rows): the whole tile is one
+// contiguous byte range of A, fetched by a single 1-D TMA bulk copy that
+// completes on the stage's mbarrier; a sub-16-byte tail (last tile only)
+// goes through cp.async.
+template <class TA>
+__device__ __forceinline__ void issue_chunk(const TtvParams &P, unsigned char *stage, uint64_t *bar, int64_t tile) {
+    const int64_t o0 = tile * P.R;
+    const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
+    const uint32_t bytes = (uint32_t)(rows * P.K * P.I * (int64_t)sizeof(TA));
+    const uint32_t b16 = bytes & ~15u;
+    const unsigned char *src = (const unsigned char *)((const TA *)P.a + o0 * P.K * P.I);
+    if (threadIdx.x == 0) {
+        fence_proxy_async_smem();  // generic reads of this buffer precede the async writes
+        mbar_arrive_expect_tx(bar, b16);
+        if (b16) bulk_g2s(stage, src, b16, bar);
+    }
+    const uint32_t tail_elems = (bytes - b16) / (uint32_t)sizeof(TA);
+    if (threadIdx.x < tail_elems)
+        cp_async<sizeof(TA)>(stage + b16 + threadIdx.x * sizeof(TA), src + b16 + threadIdx.x * sizeof(TA));
+}
+
 template <class TA, int G>
 __device__ __forceinline__ void issue_slab(const TtvParams &P, unsigned char *stage, int64_t tile, int slab) {
     const int64_t o0 = tile * P.R;
@@ -179,10 +200,11 @@ __device__ __forceinline__ void issue_slab(const TtvParams &P, unsigned char *st
     }
 }
 
-template <class TA, class TC, int G, bool VECREAD>
+template <class TA, class TC, int G, bool VECREAD, bool BULK>
 __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__ TtvParams P) {
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[kStages];
     if (stop_requested(P.stop)) return;
     const int64_t K = P.K, I = P.I;
     // b (as the accumulation type), then kStages row-padded stage buffers
@@ -193,15 +215,29 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
 
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
         bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+    if constexpr (BULK) {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    }
 
     const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t nitems = my_tiles * P.nslab;
     auto item_tile = [&](int64_t q) { return (int64_t)blockIdx.x + (q / P.nslab) * gridDim.x; };
     auto item_slab = [&](int64_t q) { return (int)(q % P.nslab); };
+    auto issue = [&](int64_t q) {
+        const int s = (int)(q % kStages);
+        if constexpr (BULK)
+            issue_chunk<TA>(P, stages + s * stage_bytes, &full_bar[s], item_tile(q));
+        else
+            issue_slab<TA, G>(P, stages + s * stage_bytes, item_tile(q), item_slab(q));
+    };
 
 #pragma unroll
     for (int q = 0; q < kStages - 1; ++q) {
-        if (q < nitems) issue_slab<TA, G>(P, stages + q * stage_bytes, item_tile(q), item_slab(q));
+        if (q < nitems) issue(q);
         cp_async_commit();
     }
 
@@ -212,10 +248,11 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
     const uint32_t outs_per_tile = (uint32_t)P.R * (uint32_t)I;
     for (int64_t q = 0; q < nitems; ++q) {
         cp_async_wait<kStages - 2>();
+        if constexpr (BULK) mbar_wait_parity(&full_bar[q % kStages], (uint32_t)((q / kStages) & 1));
         __syncthreads();
         {
             const int64_t qn = q + kStages - 1;
-            if (qn < nitems) issue_slab<TA, G>(P, stages + (qn % kStages) * stage_bytes, item_tile(qn), item_slab(qn));
+            if (qn < nitems) issue(qn);
             cp_async_commit();
         }
         const TA *st = (const TA *)(stages + (q % kStages) * stage_bytes);
@@ -293,11 +330,10 @@ struct TtvLaunch {
     int vec;
     int G;
     bool vecread;
+    bool bulk;
     dim3 grid, block;
     size_t smem;
 };
-
-static int64_t pow2_divisor(int64_t x) { return x & (-x); }
 
 // Regime-S plan: rows per tile, slab length, pitch, piece size.
 static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
@@ -319,14 +355,15 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     int64_t G = 16;
     while (G > (int64_t)s && (((K * I * s) % G) != 0 || (base_addr % G) != 0)) G /= 2;
     if (((K * I * s) % G) != 0 || (base_addr % G) != 0) G = s;
-    // slab length: stage ~24 KB
-    const int64_t stage_target = 24 * 1024;
-    int64_t Kc = std::max<int64_t>(1, stage_target / std::max<int64_t>(1, R * I * s));
-    const int64_t g_is = std::gcd(G, I * s);
-    const int64_t unit = G / g_is;  // Kc multiple of unit keeps slab offsets G-aligned
-    if (Kc >= K) {
+    // slab length: whole [K][I] rows when a tile fits the stage budget,
+    // else k-slabs whose byte offsets stay on 128-byte line boundaries
+    const int64_t stage_target = 32 * 1024;
+    int64_t Kc;
+    if (R * K * I * s <= stage_target) {
         Kc = K;
     } else {
+        const int64_t unit = std::max<int64_t>(128 / std::gcd<int64_t>(128, I * s), G / std::gcd(G, I * s));
+        Kc = stage_target / std::max<int64_t>(1, R * I * s);
         Kc = std::max<int64_t>(unit, Kc - Kc % unit);
         if (Kc >= K) Kc = K;
     }
@@ -354,6 +391,8 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     const int64_t stage_bytes = ((R * Lp * s) + 15) & ~15ll;
     const int64_t smem = bbytes + kStages * stage_bytes;
     if (smem > 200 * 1024) return false;
+    // contiguous-chunk mode: one slab, no padding -> 1-D TMA bulk copies
+    L.bulk = (Kc == K) && (Lp == L0) && (base_addr % 16 == 0) && ((R * K * I * s) % 16 == 0);
     P.R = (int32_t)R;
     P.Kc = (int32_t)Kc;
     P.Lp = (int32_t)Lp;
@@ -370,7 +409,8 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     L.vecread = vecread;
     L.block = dim3(threads);
     L.smem = (size_t)smem;
-    const int per_sm = smem <= 100 * 1024 ? 2 : 1;
+    // resident CTAs per SM from shared memory (228 KB/SM, 1 KB reserved per CTA)
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (smem + 2048)));
     const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)nsm * per_sm);
     L.grid = dim3((unsigned)grid);
     return true;
@@ -423,12 +463,16 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         kern<<<L.grid, L.block, L.smem, st>>>(L.P);
         return cudaGetLastError();
     };
-    if (L.vecread) return go(ttv_staged_kernel<TA, TC, 16, true>);
+    if (L.bulk) {
+        if (L.vecread) return go(ttv_staged_kernel<TA, TC, 16, true, true>);
+        return go(ttv_staged_kernel<TA, TC, 16, false, true>);
+    }
+    if (L.vecread) return go(ttv_staged_kernel<TA, TC, 16, true, false>);
     switch (L.G) {
-        case 16: return go(ttv_staged_kernel<TA, TC, 16, false>);
-        case 8: return go(ttv_staged_kernel<TA, TC, 8, false>);
+        case 16: return go(ttv_staged_kernel<TA, TC, 16, false, false>);
+        case 8: return go(ttv_staged_kernel<TA, TC, 8, false, false>);
         default:
-            if constexpr (sizeof(TA) == 4) return go(ttv_staged_kernel<TA, TC, 4, false>);
+            if constexpr (sizeof(TA) == 4) return go(ttv_staged_kernel<TA, TC, 4, false, false>);
             return cudaErrorInvalidValue;
     }
 }

@@ -79,10 +79,16 @@ class DenseTensor:
     __slots__ = ("meta", "buffer")
 
     def __init__(self, shape, offsets=None, layout=None, fill_value=0, dtype=None, device=None):
+        """Value-initialised like the reference (tensor.py:44-46).
+        ``fill_value=None`` leaves the buffer uninitialised (contraction
+        outputs, which the kernels overwrite completely)."""
         self.meta = TensorMeta(shape, offsets, layout)
         dt = as_dtype(dtype)
         dev = torch.device(device) if device is not None else _default_device()
-        self.buffer = torch.full((self.meta.size,), fill_value, dtype=dt, device=dev)
+        if fill_value is None:
+            self.buffer = torch.empty((self.meta.size,), dtype=dt, device=dev)
+        else:
+            self.buffer = torch.full((self.meta.size,), fill_value, dtype=dt, device=dev)
 
     # -- construction -------------------------------------------------------------
     @classmethod

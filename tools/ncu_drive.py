@@ -1,0 +1,79 @@
+"""Drive exactly one launch of each hot kernel inside a cudaProfilerStart/Stop
+window, for `ncu --profile-from-start off` captures:
+
+    python tools/ncu_drive.py [cfg2] [cfg3] [cfg5] [cfg4]
+    ncu --profile-from-start off --set full --clock-control none --import-source on \
+        -o gpurun_out/prof python tools/ncu_drive.py cfg2
+"""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import torch
+
+import paper_1711_10912_b200 as tl
+import paper_1711_10912_b200.contraction as C
+import workloads as W
+
+
+def main(which):
+    ops = []
+    keep = []
+    if "cfg2" in which:
+        T, vecs, T2 = W.cfg2()
+        vs = [tl.DenseTensor.from_memory((128,), v) for v in vecs]
+        As = {n: tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, l), layout=l) for n, l in W.CFG2_LAYOUTS.items()}
+        B = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T2, (1, 2, 3, 4)))
+        keep += [As, B, vs]
+        for n in W.CFG2_LAYOUTS:
+            for m in (1, 2, 3, 4):
+                ops.append(lambda A=As[n], m=m: tl.ttv(A, vs[m - 1], m))
+        ops.append(lambda: C.frobenius_norm_device(As["first"]))
+        ops.append(lambda: C.inner_product_device(As["first"], B))
+        del T, T2
+    if "cfg3" in which:
+        A_, B_ = W.cfg3()
+        A3 = tl.DenseTensor.from_memory(A_.shape, W.layout_buffer(A_, (1, 2, 3)))
+        A3l = tl.DenseTensor.from_memory(A_.shape, W.layout_buffer(A_, (3, 2, 1)), layout=(3, 2, 1))
+        Bm = tl.DenseTensor.from_memory(B_.shape, W.layout_buffer(B_, (1, 2)))
+        keep += [A3, A3l, Bm]
+        ops.append(lambda: tl.ttm(A3, Bm, 2))
+        ops.append(lambda: tl.ttm(A3l, Bm, 2))
+        del A_
+    if "cfg5" in which:
+        for seed in (0, 5):
+            T, v, M, layout = W.cfg5(seed)
+            A5 = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, layout), layout=layout)
+            V = tl.DenseTensor.from_memory((9,), v)
+            Bm5 = tl.DenseTensor.from_memory(M.shape, W.layout_buffer(M, (1, 2)))
+            C1 = tl.ttv(A5, V, 5)
+            C2 = tl.ttm(C1, Bm5, 2)
+            keep += [A5, V, Bm5, C1, C2]
+            ops.append(lambda A5=A5, V=V: tl.ttv(A5, V, 5))
+            ops.append(lambda C1=C1, Bm5=Bm5: tl.ttm(C1, Bm5, 2))
+            ops.append(lambda C2=C2: C.frobenius_norm_device(C2))
+            del T
+    if "cfg4" in which:
+        T, _ = W.cfg4()
+        A4 = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, (1, 2, 3)))
+        r = tl.HopmRunner(A4, max_sweeps=2, tol=0.0)
+        keep += [A4, r]
+        ops.append(r.launch)
+        del T
+    for op in ops:  # warm (module load, planning)
+        op()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    for op in ops:
+        op()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print("ok", len(ops), "ops")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["cfg2"])

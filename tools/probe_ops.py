@@ -17,7 +17,33 @@ import workloads as W
 HBM = 6456.2
 
 
-def timeit(fn, iters=10, warm=3):
+def timeit(fn, iters=10, warm=3, reps=8):
+    """Device time per call: `reps` calls in one CUDA graph (no host overhead)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(warm):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / reps)
+    del g
+    return float(np.median(ts)), float(np.min(ts))
+
+
+def timeit_eager(fn, iters=10, warm=3):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -76,7 +102,7 @@ def main(which):
         T, _ = W.cfg4()
         A = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, (1, 2, 3)))
         r = tl.HopmRunner(A, max_sweeps=50, tol=0.0)
-        med, mn = timeit(r.launch, iters=5, warm=2)
+        med, mn = timeit_eager(r.launch, iters=5, warm=2)
         print(f"cfg4 hopm 50 sweeps: {med:.3f} ms -> {50/med*1e3:.0f} sweeps/s; 2-pass bytes frac "
               f"{2*8*64e6*50/(med*1e-3)/1e9/HBM:.2f}", flush=True)
         st = r.state()
@@ -88,7 +114,7 @@ def main(which):
             A = tl.DenseTensor.from_memory(A_.shape, W.layout_buffer(A_, layout), layout=layout)
             Bm = tl.DenseTensor.from_memory(B_.shape, W.layout_buffer(B_, (1, 2)))
             for mode in (1, 2, 3):
-                med, _ = timeit(lambda: tl.ttm(A, Bm, mode), iters=3, warm=1)
+                med, _ = timeit_eager(lambda: tl.ttm(A, Bm, mode), iters=3, warm=1)
                 fl = 2 * 512**3 * 384
                 print(f"cfg3 ttm {layout} q={mode}: {med:.3f} ms {fl/med/1e9:.2f} TFLOP/s", flush=True)
             del A

@@ -72,13 +72,18 @@ __device__ __forceinline__ void cp_async8_zfill(void *smem_dst, const void *gmem
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(n));
 }
 
+__device__ __forceinline__ void cp_async16_zfill(void *smem_dst, const void *gmem_src, bool valid) {
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(n));
+}
+
 __device__ __forceinline__ void mma_16x8x4(double (&d)[4], const double (&a)[2], double b) {
     asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
                  : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
                  : "d"(a[0]), "d"(a[1]), "d"(b));
 }
 
-template <class CFG, bool A_KMAJOR, bool B_KMAJOR>
+template <class CFG, bool A_KMAJOR, bool B_KMAJOR, bool PAIRS>
 __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_constant__ TtmParams P) {
     using namespace gett;
     constexpr int THREADS = CFG::THREADS, TM = CFG::TM, TN = CFG::TN, WN = CFG::WN;
@@ -137,36 +142,75 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
     const double *b_base_fixed = P.b + (m0 + b_mm0) * P.bs0;
     const bool b_row_ok = (m0 + b_mm0) < P.J;
 
+    // 16-byte variant: pairs of elements adjacent in both global and shared
+    // memory (along n / m for N-major, along k for K-major), half the LDGSTS
+    constexpr int LPT2 = LPT / 2;
+    const int a_p0 = A_KMAJOR ? 2 * (tid & (BK / 2 - 1)) : 2 * (tid & (BN / 2 - 1));  // element index of pair
+    const int a_q0 = A_KMAJOR ? tid / (BK / 2) : tid / (BN / 2);
+    const int b_p0 = B_KMAJOR ? 2 * (tid & (BK / 2 - 1)) : 2 * (tid & (BM / 2 - 1));
+    const int b_q0 = B_KMAJOR ? tid / (BK / 2) : tid / (BM / 2);
+
     auto load_stage = [&](int stage, int kt) {
         const int64_t k0 = (int64_t)kt * BK;
         double *as = As + stage * A_TILE;
         double *bs = Bs + stage * B_TILE;
+        if constexpr (PAIRS) {
 #pragma unroll
-        for (int s = 0; s < LPT; ++s) {
-            if constexpr (A_KMAJOR) {
-                const int nn = a_nn0 + s * (THREADS / BK);
-                const int64_t k = k0 + a_kk0;
-                const bool ok = (k < K) && (coff[nn] >= 0);
-                cp_async8_zfill(as + nn * LDK + a_kk0, P.a + (ok ? aoff[nn] + k : 0), ok);
-            } else {
-                const int kk = a_kk0 + s * (THREADS / BN);
-                const int64_t k = k0 + kk;
-                const bool ok = a_col_ok && (k < K);
-                cp_async8_zfill(as + kk * LDW + a_nn0, ok ? a_base_fixed + k * I : P.a, ok);
+            for (int s = 0; s < LPT2; ++s) {
+                if constexpr (A_KMAJOR) {  // pair (k, k+1) of column nn
+                    const int nn = a_q0 + s * (THREADS / (BK / 2));
+                    const int64_t k = k0 + a_p0;
+                    const bool ok = (k < K) && (coff[nn] >= 0);
+                    cp_async16_zfill(as + nn * LDK + a_p0, P.a + (ok ? aoff[nn] + k : 0), ok);
+                } else {  // pair (n, n+1) of row kk
+                    const int kk = a_q0 + s * (THREADS / (BN / 2));
+                    const int64_t k = k0 + kk;
+                    const bool ok = (k < K) && (coff[a_p0] >= 0);
+                    cp_async16_zfill(as + kk * LDW + a_p0, P.a + (ok ? aoff[a_p0] + k * I : 0), ok);
+                }
             }
-        }
 #pragma unroll
-        for (int s = 0; s < LPT; ++s) {
-            if constexpr (B_KMAJOR) {
-                const int mm = b_mm0 + s * (THREADS / BK);
-                const int64_t k = k0 + b_kk0, j = m0 + mm;
-                const bool ok = (k < K) && (j < P.J);
-                cp_async8_zfill(bs + mm * LDK + b_kk0, P.b + (ok ? j * P.bs0 + k : 0), ok);
-            } else {
-                const int kk = b_kk0 + s * (THREADS / BM);
-                const int64_t k = k0 + kk;
-                const bool ok = b_row_ok && (k < K);
-                cp_async8_zfill(bs + kk * LDW + b_mm0, ok ? b_base_fixed + k * P.bs1 : P.b, ok);
+            for (int s = 0; s < LPT2; ++s) {
+                if constexpr (B_KMAJOR) {
+                    const int mm = b_q0 + s * (THREADS / (BK / 2));
+                    const int64_t k = k0 + b_p0, j = m0 + mm;
+                    const bool ok = (k < K) && (j < P.J);
+                    cp_async16_zfill(bs + mm * LDK + b_p0, P.b + (ok ? j * P.bs0 + k : 0), ok);
+                } else {
+                    const int kk = b_q0 + s * (THREADS / (BM / 2));
+                    const int64_t k = k0 + kk, j = m0 + b_p0;
+                    const bool ok = (k < K) && (j < P.J);
+                    cp_async16_zfill(bs + kk * LDW + b_p0, P.b + (ok ? j + k * P.bs1 : 0), ok);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < LPT; ++s) {
+                if constexpr (A_KMAJOR) {
+                    const int nn = a_nn0 + s * (THREADS / BK);
+                    const int64_t k = k0 + a_kk0;
+                    const bool ok = (k < K) && (coff[nn] >= 0);
+                    cp_async8_zfill(as + nn * LDK + a_kk0, P.a + (ok ? aoff[nn] + k : 0), ok);
+                } else {
+                    const int kk = a_kk0 + s * (THREADS / BN);
+                    const int64_t k = k0 + kk;
+                    const bool ok = a_col_ok && (k < K);
+                    cp_async8_zfill(as + kk * LDW + a_nn0, ok ? a_base_fixed + k * I : P.a, ok);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < LPT; ++s) {
+                if constexpr (B_KMAJOR) {
+                    const int mm = b_mm0 + s * (THREADS / BK);
+                    const int64_t k = k0 + b_kk0, j = m0 + mm;
+                    const bool ok = (k < K) && (j < P.J);
+                    cp_async8_zfill(bs + mm * LDK + b_kk0, P.b + (ok ? j * P.bs0 + k : 0), ok);
+                } else {
+                    const int kk = b_kk0 + s * (THREADS / BM);
+                    const int64_t k = k0 + kk;
+                    const bool ok = b_row_ok && (k < K);
+                    cp_async8_zfill(bs + kk * LDW + b_mm0, ok ? b_base_fixed + k * P.bs1 : P.b, ok);
+                }
             }
         }
     };
@@ -255,14 +299,6 @@ struct Digit {
     int64_t ext, as, cs;  // extent, A stride, C stride
 };
 
-static int gett_variant() {
-    static int v = [] {
-        const char *e = getenv("TL_GETT_WARPS");
-        return (e && atoi(e) == 8) ? 8 : 16;
-    }();
-    return v;
-}
-
 int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
                      cudaStream_t st) {
     using namespace gett;
@@ -343,20 +379,30 @@ int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     const int64_t grid = ntiles * P.mtiles;
     if (grid > 0x7fffffffll) return TL_EUNSUPPORTED;
     const bool b_kmajor = (bm.stride[1] == 1 && bm.extent[1] > 1);
-    auto go = [&](auto kern, int threads) -> int {
+    // 16-byte operand pairs: both elements of every pair adjacent in global
+    // memory, 16-byte aligned, and never straddling a masked column
+    const uintptr_t pa = (uintptr_t)P.a, pb = (uintptr_t)P.b;
+    bool pairs = (pa % 16 == 0) && (pb % 16 == 0);
+    if (a_kmajor)
+        pairs = pairs && (cn.K % 2 == 0);
+    else
+        pairs = pairs && sigma[0].as == 1 && sigma[0].ext % 2 == 0 && F % 2 == 0 && cn.I % 2 == 0;
+    if (b_kmajor)
+        pairs = pairs && (cn.K % 2 == 0) && (P.bs0 % 2 == 0);
+    else
+        pairs = pairs && (P.bs0 == 1) && (J % 2 == 0) && (P.bs1 % 2 == 0);
+    auto go = [&](auto kern) -> int {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
         if (e != cudaSuccess) return cuda_status(e, "ttm smem attribute");
-        kern<<<(unsigned)grid, threads, SMEM, st>>>(P);
+        kern<<<(unsigned)grid, Cfg16::THREADS, SMEM, st>>>(P);
         return cuda_status(cudaGetLastError(), "ttm dmma launch");
     };
-    if (gett_variant() == 8) {
-        constexpr int T = Cfg8::THREADS;
-        if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg8, true, true>, T) : go(ttm_dmma_kernel<Cfg8, true, false>, T);
-        return b_kmajor ? go(ttm_dmma_kernel<Cfg8, false, true>, T) : go(ttm_dmma_kernel<Cfg8, false, false>, T);
+    if (pairs) {
+        if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg16, true, true, true>) : go(ttm_dmma_kernel<Cfg16, true, false, true>);
+        return b_kmajor ? go(ttm_dmma_kernel<Cfg16, false, true, true>) : go(ttm_dmma_kernel<Cfg16, false, false, true>);
     }
-    constexpr int T = Cfg16::THREADS;
-    if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg16, true, true>, T) : go(ttm_dmma_kernel<Cfg16, true, false>, T);
-    return b_kmajor ? go(ttm_dmma_kernel<Cfg16, false, true>, T) : go(ttm_dmma_kernel<Cfg16, false, false>, T);
+    if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg16, true, true, false>) : go(ttm_dmma_kernel<Cfg16, true, false, false>);
+    return b_kmajor ? go(ttm_dmma_kernel<Cfg16, false, true, false>) : go(ttm_dmma_kernel<Cfg16, false, false, false>);
 }
 
 }  // namespace tl

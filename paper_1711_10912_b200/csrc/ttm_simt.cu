@@ -14,6 +14,7 @@
 //
 // ttm_simt: one thread per output, the reference's fold (fallback).
 #include <algorithm>
+#include <cstdlib>
 
 #include "plan.h"
 #include "tl_common.cuh"
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(256) ttm_simt_kernel(const __grid_constant__ T
 }
 
 // ------------------------------------------------------------ staged (small J)
-constexpr int kTtmStages = 4;
+constexpr int kTtmStages = 3;
 constexpr int kJB = 16;
 
 template <class T> __device__ __forceinline__ typename AccOf<T>::type mac(typename AccOf<T>::type acc, T a, typename AccOf<T>::type b);
@@ -92,8 +93,10 @@ __device__ __forceinline__ void mma_16x8x4_s(double (&d)[4], double a0, double a
                  : "d"(a0), "d"(a1), "d"(b));
 }
 
-template <class T, bool DMMA>
+// MT = 0: SIMT fold; MT = 1, 2: FP64 DMMA with MT m16 tiles (J <= 16 MT)
+template <class T, int MT, int NTILE = 4>
 __global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__ TtmSimtParams P) {
+    constexpr bool DMMA = MT > 0;
     using Acc = typename AccOf<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[kTtmStages];
@@ -173,57 +176,53 @@ __global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__
             // (jpad/16 m16 tiles); k in steps of 4 with zero padding
             const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
             const int g = lane >> 2, t = lane & 3;
-            const int64_t ldb = ttm_ldb(K);
-            const int mtiles = (int)(jpad / 16);
-            for (uint32_t p0 = warp * 32; p0 < slots; p0 += nw * 32) {
-                // this lane's B-fragment column positions (n = g) for the 4 tiles
-                int64_t base[4];
-                bool okp[4];
+            const int ldb = (int)ttm_ldb(K);
+            constexpr int NT = NTILE;  // n8 tiles per warp: NT x MT independent MMA chains
+            for (uint32_t p0 = warp * (8 * NT); p0 < slots; p0 += nw * (8 * NT)) {
+                // this lane's B-fragment column positions (n = g) per tile
+                int base[NT];
+                bool okp[NT];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
+                for (int nt = 0; nt < NT; ++nt) {
                     uint32_t r, i;
                     const uint32_t pos = p0 + nt * 8 + g;
                     P.I_div.divmod(pos, r, i);
                     okp[nt] = pos < slots && r < rows;
-                    base[nt] = (int64_t)r * KI + i;
+                    base[nt] = okp[nt] ? (int)(r * KI + i) : 0;
                 }
-                for (int mt = 0; mt < mtiles; mt += 4) {
-                    double acc[4][4][4];
+                double acc[MT][NT][4];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                for (int a = 0; a < MT; ++a)
 #pragma unroll
-                        for (int b = 0; b < 4; ++b)
+                    for (int b = 0; b < NT; ++b)
 #pragma unroll
-                            for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
-                    for (int64_t k4 = 0; k4 < K; k4 += 4) {
-                        const int64_t k = k4 + t;
-                        double bf[4];
+                        for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+                const double *brow = (const double *)bsm + g * ldb + t;
+                for (int k4 = 0; k4 < (int)K; k4 += 4) {
+                    const int k = k4 + t;
+                    const bool kok = k < (int)K;
+                    double bf[NT];
 #pragma unroll
-                        for (int nt = 0; nt < 4; ++nt)
-                            bf[nt] = (okp[nt] && k < K) ? (double)st[base[nt] + k * I] : 0.0;
+                    for (int nt = 0; nt < NT; ++nt) bf[nt] = (okp[nt] && kok) ? (double)st[base[nt] + k * (int)I] : 0.0;
 #pragma unroll
-                        for (int mm = 0; mm < 4; ++mm) {
-                            if (mt + mm >= mtiles) break;
-                            const double *brow = (const double *)bsm + ((mt + mm) * 16 + g) * ldb + k4 + t;
-                            const double a0 = brow[0], a1 = brow[8 * ldb];
+                    for (int mm = 0; mm < MT; ++mm) {
+                        const double a0 = brow[(mm * 16) * ldb + k4], a1 = brow[(mm * 16 + 8) * ldb + k4];
 #pragma unroll
-                            for (int nt = 0; nt < 4; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
-                        }
+                        for (int nt = 0; nt < NT; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
                     }
+                }
 #pragma unroll
-                    for (int mm = 0; mm < 4; ++mm) {
-                        if (mt + mm >= mtiles) break;
+                for (int mm = 0; mm < MT; ++mm) {
 #pragma unroll
-                        for (int nt = 0; nt < 4; ++nt) {
+                    for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                const uint32_t pos = p0 + nt * 8 + 2 * t + (v & 1);
-                                const int64_t j = (mt + mm) * 16 + g + 8 * (v >> 1);
-                                if (pos < slots) {
-                                    uint32_t r, i;
-                                    P.I_div.divmod(pos, r, i);
-                                    put(r, i, j, (Acc)acc[mm][nt][v]);
-                                }
+                        for (int v = 0; v < 4; ++v) {
+                            const uint32_t pos = p0 + nt * 8 + 2 * t + (v & 1);
+                            const int64_t j = mm * 16 + g + 8 * (v >> 1);
+                            if (pos < slots) {
+                                uint32_t r, i;
+                                P.I_div.divmod(pos, r, i);
+                                put(r, i, j, (Acc)acc[mm][nt][v]);
                             }
                         }
                     }
@@ -302,7 +301,16 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
     if (P.O * P.I == 0) return TL_OK;
     if (P.I > 256 || KI * s > 32 * 1024 || P.J * P.K * 8 > 48 * 1024 || base % 16 != 0 || P.O > 0xffffffffll)
         return TL_EUNSUPPORTED;
-    const int64_t stage_target = 20 * 1024;
+    static const int64_t stage_kb = [] {
+        const char *e = getenv("TL_TTM_STAGE_KB");
+        return (int64_t)(e ? atoi(e) : 28);
+    }();
+    static const int ntile = [] {
+        const char *e = getenv("TL_TTM_NT");
+        return e ? atoi(e) : 4;
+    }();
+    static const bool force_simt = getenv("TL_TTM_SIMT") != nullptr;
+    const int64_t stage_target = stage_kb * 1024;
     int64_t R = std::max<int64_t>(1, std::min<int64_t>(256 / P.I, stage_target / (KI * s)));
     // keep every tile's start 16-byte aligned for the bulk copy
     while (R > 1 && (R * KI * s) % 16 != 0) --R;
@@ -310,8 +318,11 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
     P.R = (int32_t)R;
     P.ntiles = (P.O + R - 1) / R;
     P.I_div.init((uint32_t)P.I);
-    const bool dmma = (a.dtype == TL_F64);  // FP64 tensor cores for float64
-    const int threads = (int)std::min<int64_t>(256, std::max<int64_t>(32, ((R * P.I + 31) / 32) * 32));
+    const bool dmma = (a.dtype == TL_F64) && P.J <= 32 && !force_simt;  // FP64 tensor cores for float64
+    // SIMT: one position per thread; DMMA: 8*NT positions per warp
+    const int64_t per_thread = dmma ? ntile / 4 : 1;
+    const int threads =
+        (int)std::min<int64_t>(256, std::max<int64_t>(32, ((R * P.I + 32 * per_thread - 1) / (32 * per_thread)) * 32));
     const size_t bbytes = dmma ? StagedLayout<double, true>(P.J, P.K).bbytes
                                : (a.dtype == TL_F32 ? StagedLayout<float, false>(P.J, P.K).bbytes
                                                     : StagedLayout<int64_t, false>(P.J, P.K).bbytes);
@@ -327,9 +338,11 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
         kern<<<(unsigned)grid, threads, smem, st>>>(P);
         return cuda_status(cudaGetLastError(), "ttm staged launch");
     };
-    if (dmma) return go(ttm_staged_kernel<double, true>);
-    if (a.dtype == TL_F32) return go(ttm_staged_kernel<float, false>);
-    return go(ttm_staged_kernel<int64_t, false>);
+    if (dmma && ntile == 8) return P.J <= 16 ? go(ttm_staged_kernel<double, 1, 8>) : go(ttm_staged_kernel<double, 2, 8>);
+    if (dmma) return P.J <= 16 ? go(ttm_staged_kernel<double, 1, 4>) : go(ttm_staged_kernel<double, 2, 4>);
+    if (a.dtype == TL_F64) return go(ttm_staged_kernel<double, 0>);
+    if (a.dtype == TL_F32) return go(ttm_staged_kernel<float, 0>);
+    return go(ttm_staged_kernel<int64_t, 0>);
 }
 
 int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,

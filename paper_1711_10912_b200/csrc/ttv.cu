@@ -189,14 +189,26 @@ __device__ __forceinline__ void issue_slab(const TtvParams &P, unsigned char *st
     const bool tail = (kc != P.Kc);
     const FastDiv &pr = tail ? P.pr_tail : P.pr_div;
     const uint32_t pieces_row = pr.d;
-    const uint32_t total = rows * pieces_row;
     const unsigned char *src0 = (const unsigned char *)((const TA *)P.a + (o0 * P.K + k0) * P.I);
     const int64_t grow = P.K * P.I * (int64_t)sizeof(TA);  // global row pitch, bytes
     const uint32_t srow = (uint32_t)P.Lp * (uint32_t)sizeof(TA);  // smem row pitch, bytes
-    for (uint32_t p = threadIdx.x; p < total; p += blockDim.x) {
+    if (blockDim.x % pieces_row == 0) {
+        // each thread owns one piece column and walks rows: no division
+        const uint32_t rstep = blockDim.x / pieces_row;
         uint32_t r, cpc;
-        pr.divmod(p, r, cpc);
-        cp_async<G>(stage + r * srow + cpc * G, src0 + (int64_t)r * grow + (int64_t)cpc * G);
+        pr.divmod(threadIdx.x, r, cpc);
+        const unsigned char *src = src0 + (int64_t)r * grow + (int64_t)cpc * G;
+        unsigned char *dst = stage + r * srow + cpc * G;
+        const int64_t gstep = (int64_t)rstep * grow;
+        const uint32_t sstep = rstep * srow;
+        for (; r < rows; r += rstep, src += gstep, dst += sstep) cp_async<G>(dst, src);
+    } else {
+        const uint32_t total = rows * pieces_row;
+        for (uint32_t p = threadIdx.x; p < total; p += blockDim.x) {
+            uint32_t r, cpc;
+            pr.divmod(p, r, cpc);
+            cp_async<G>(stage + r * srow + cpc * G, src0 + (int64_t)r * grow + (int64_t)cpc * G);
+        }
     }
 }
 
@@ -223,21 +235,27 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
         __syncthreads();
     }
 
+    // Work items are (tile, slab) pairs in order; the producer runs
+    // kStages-1 items ahead.  Both walk them with counters (no division).
     const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t nitems = my_tiles * P.nslab;
-    auto item_tile = [&](int64_t q) { return (int64_t)blockIdx.x + (q / P.nslab) * gridDim.x; };
-    auto item_slab = [&](int64_t q) { return (int)(q % P.nslab); };
-    auto issue = [&](int64_t q) {
-        const int s = (int)(q % kStages);
+    int64_t p_tile = blockIdx.x;  // producer position
+    int p_slab = 0, p_stage = 0;
+    auto issue_next = [&]() {
         if constexpr (BULK)
-            issue_chunk<TA>(P, stages + s * stage_bytes, &full_bar[s], item_tile(q));
+            issue_chunk<TA>(P, stages + p_stage * stage_bytes, &full_bar[p_stage], p_tile);
         else
-            issue_slab<TA, G>(P, stages + s * stage_bytes, item_tile(q), item_slab(q));
+            issue_slab<TA, G>(P, stages + p_stage * stage_bytes, p_tile, p_slab);
+        if (++p_slab == P.nslab) {
+            p_slab = 0;
+            p_tile += gridDim.x;
+        }
+        if (++p_stage == kStages) p_stage = 0;
     };
 
 #pragma unroll
     for (int q = 0; q < kStages - 1; ++q) {
-        if (q < nitems) issue(q);
+        if (q < nitems) issue_next();
         cp_async_commit();
     }
 
@@ -246,18 +264,16 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
     for (int t = 0; t < kMaxOpt; ++t) acc[t] = Acc(0);
 
     const uint32_t outs_per_tile = (uint32_t)P.R * (uint32_t)I;
+    int64_t tile = blockIdx.x;  // consumer position
+    int slab = 0, c_stage = 0;
+    uint32_t parity = 0;
     for (int64_t q = 0; q < nitems; ++q) {
         cp_async_wait<kStages - 2>();
-        if constexpr (BULK) mbar_wait_parity(&full_bar[q % kStages], (uint32_t)((q / kStages) & 1));
+        if constexpr (BULK) mbar_wait_parity(&full_bar[c_stage], parity);
         __syncthreads();
-        {
-            const int64_t qn = q + kStages - 1;
-            if (qn < nitems) issue(qn);
-            cp_async_commit();
-        }
-        const TA *st = (const TA *)(stages + (q % kStages) * stage_bytes);
-        const int64_t tile = item_tile(q);
-        const int slab = item_slab(q);
+        if (q + kStages - 1 < nitems) issue_next();
+        cp_async_commit();
+        const TA *st = (const TA *)(stages + c_stage * stage_bytes);
         const int64_t k0 = (int64_t)slab * P.Kc;
         const int kc = (int)((K - k0 < P.Kc) ? K - k0 : P.Kc);
         const int64_t o0 = tile * P.R;
@@ -279,10 +295,12 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
                 for (int kk = 0; kk < kc; kk += E) {
                     if constexpr (E == 4) {
                         const float4 v = *(const float4 *)(row + kk);
-                        a_ = fold_step(a_, (Acc)v.x, bs[k0 + kk + 0]);
-                        a_ = fold_step(a_, (Acc)v.y, bs[k0 + kk + 1]);
-                        a_ = fold_step(a_, (Acc)v.z, bs[k0 + kk + 2]);
-                        a_ = fold_step(a_, (Acc)v.w, bs[k0 + kk + 3]);
+                        const double2 b01 = *(const double2 *)(bs + k0 + kk);
+                        const double2 b23 = *(const double2 *)(bs + k0 + kk + 2);
+                        a_ = fold_step(a_, (Acc)v.x, b01.x);
+                        a_ = fold_step(a_, (Acc)v.y, b01.y);
+                        a_ = fold_step(a_, (Acc)v.z, b23.x);
+                        a_ = fold_step(a_, (Acc)v.w, b23.y);
                     } else {
                         union { uint4 raw; TA v[2]; } u;
                         u.raw = *(const uint4 *)(row + kk);
@@ -318,6 +336,14 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
                 }
                 acc[t] = Acc(0);
             }
+        }
+        if (++slab == P.nslab) {
+            slab = 0;
+            tile += gridDim.x;
+        }
+        if (++c_stage == kStages) {
+            c_stage = 0;
+            parity ^= 1u;
         }
     }
     cp_async_wait<0>();

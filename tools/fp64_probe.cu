@@ -143,6 +143,28 @@ int main() {
             printf("DMMA %-9s warps/SM %2d: %.2f TFLOP/s\n", names[s], wpb, flops / ms / 1e9);
         }
     }
+    // sustained DMMA: back-to-back launches for ~4 s (power/clock steady state)
+    {
+        const int wpb = 8, iters = 4000;
+        double flops1 = 2.0 * 16 * 8 * 8 * 8 * iters * (double)nsm * wpb;
+        cudaEventRecord(e0);
+        int launches = 0;
+        double ms = 0;
+        while (ms < 4000.0) {
+            for (int r = 0; r < 20; ++r) dmma_tput<2><<<nsm, wpb * 32>>>(out, iters);
+            launches += 20;
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            ms = now_ms(e0, e1);
+        }
+        // last window
+        cudaEventRecord(e0);
+        for (int r = 0; r < 40; ++r) dmma_tput<2><<<nsm, wpb * 32>>>(out, iters);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        double ms2 = now_ms(e0, e1);
+        printf("DMMA m16n8k8 sustained (after %.1f s): %.2f TFLOP/s\n", ms / 1e3, 40 * flops1 / ms2 / 1e9);
+    }
     // DMMA semantics: compare with sequential fma chain and mul+add chain
     {
         double hA[32], hB[32], hC[64], hD[64];

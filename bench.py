@@ -119,7 +119,8 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- distributed
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, backend="nccl"):
+    """One process per GPU (torchrun env); returns (world, rank, local_rank)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -128,20 +129,30 @@ def dist_setup(n_gpus):
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
 def dist_max(x, world):
+    """Max over ranks (the step time of a weak-scaled run is the slowest rank's)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_value(step_bytes, world, ms_max):
+    """Whole-job throughput of `world` independent replicas, GB/s."""
+    return world * step_bytes / (ms_max * 1e-3) / 1e9
 
 
 def barrier(world):
@@ -496,7 +507,7 @@ def main():
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = dist_max(ms_local, world)
     ttv_ms = ev.mean_ms()
-    value = world * STEP_BYTES / (ms * 1e-3) / 1e9
+    value = replica_value(STEP_BYTES, world, ms)
 
     # end to end through the public API (pinned host buffers, copies inside)
     e2e = None

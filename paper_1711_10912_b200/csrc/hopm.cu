@@ -23,19 +23,15 @@
 // division -- so lambda history and vectors match the reference bit for bit.
 #include <vector>
 
+#include "hopm_norm.cuh"
 #include "plan.h"
 #include "tl_common.cuh"
 
 namespace tl {
 
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
-                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st);
-
-struct HopmCtl {
-    int32_t stop;
-    int32_t have_prev;
-    double prev;
-};
+                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
+                const FusedNorm *fn);
 
 constexpr int kNormSmem = 6000;  // doubles staged in shared memory for the norm fold
 
@@ -209,6 +205,20 @@ int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, d
                     first_k = mode1 - 1;
                 }
                 bool use_ping = true;
+                const int last_k = (mode1 == 1) ? 2 : 1;  // final contraction of this chain
+                // the normalisation is fused into the final ttv (its last CTA)
+                FusedNorm fn{};
+                fn.enabled = (n <= kNormSmem) ? 1 : 0;
+                fn.r = r;
+                fn.p = p;
+                fn.sweep = sweep;
+                fn.n = n;
+                fn.tol = tol;
+                fn.u = u[r];
+                fn.l = l;
+                fn.hist = hist;
+                fn.info = info;
+                fn.ctl = ctl;
                 for (int k = first_k; k >= 1; --k) {
                     if (k == mode1) continue;
                     // output: cur with dimension k removed, first-order float64
@@ -223,11 +233,13 @@ int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, d
                         out = use_ping ? (void *)ping : (void *)pong;
                         use_ping = !use_ping;
                     }
-                    int rc = ttv_enqueue(cur, cur_ptr, u[k - 1], TL_F64, 1, TL_F64, out, k - 1, stop, st);
+                    int rc = ttv_enqueue(cur, cur_ptr, u[k - 1], TL_F64, 1, TL_F64, out, k - 1, stop, st,
+                                         k == last_k ? &fn : nullptr);
                     if (rc != TL_OK) return rc;
                     cur = first_order_desc(q, shp, TL_F64);
                     cur_ptr = out;
                 }
+                if (fn.enabled) continue;
                 wsrc.ptr = cur_ptr;
                 wsrc.dtype = TL_F64;
                 wsrc.stride = 1;

@@ -24,6 +24,7 @@
 #include <numeric>
 #include <type_traits>
 
+#include "hopm_norm.cuh"
 #include "plan.h"
 #include "tl_common.cuh"
 
@@ -34,6 +35,7 @@ struct TtvParams {
     const void *b;
     void *c;
     const int32_t *stop;  // optional device flag: skip all work when set (HOPM)
+    FusedNorm fn;         // optional HOPM normalisation of the output (last CTA)
     int64_t b_stride;
     int32_t b_dtype;
     int32_t b_smem;  // stage b in shared memory
@@ -123,35 +125,101 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
     }
     const int64_t IV = I / VEC;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= P.O * IV) return;
-    const int64_t o = gid / IV;
-    const int64_t i0 = (gid - o * IV) * VEC;
-    const TA *pa = (const TA *)P.a + (o * K) * I + i0;
+    if (gid < P.O * IV) {
+        const int64_t o = gid / IV;
+        const int64_t i0 = (gid - o * IV) * VEC;
+        const TA *pa = (const TA *)P.a + (o * K) * I + i0;
 
-    Acc acc[VEC];
+        Acc acc[VEC];
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) acc[j] = Acc(0);
+        for (int j = 0; j < VEC; ++j) acc[j] = Acc(0);
 
-    int64_t k = 0;
-    for (; k + U <= K; k += U) {
-        Acc v[U][VEC];
+        int64_t k = 0;
+        for (; k + U <= K; k += U) {
+            Acc v[U][VEC];
 #pragma unroll
-        for (int u = 0; u < U; ++u) VecLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
+            for (int u = 0; u < U; ++u) VecLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const Acc bk = P.b_smem ? bs[k + u] : load_elem_as<Acc>(P.b, P.b_dtype, (k + u) * P.b_stride);
+            for (int u = 0; u < U; ++u) {
+                const Acc bk = P.b_smem ? bs[k + u] : load_elem_as<Acc>(P.b, P.b_dtype, (k + u) * P.b_stride);
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[u][j], bk);
+                for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[u][j], bk);
+            }
+        }
+        for (; k < K; ++k) {
+            Acc v[VEC];
+            VecLoad<TA, VEC>::ld(pa + k * I, v);
+            const Acc bk = P.b_smem ? bs[k] : load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[j], bk);
+        }
+        store_outputs<TC, VEC>(P, o, i0, acc);
+    }
+    if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
+}
+
+// ------------------------------------------------------------- column blocks
+// Strided fibers with few outputs (O*I small, e.g. HOPM's 400x400
+// intermediates): one CTA per (o, 32 consecutive i); 128 threads stream
+// k-slabs of the [K][32] column block into shared memory (4-stage cp.async),
+// warp 0 folds its 32 columns in k order.  Latency-bound by design: the
+// whole column block is in flight at once instead of one load per fold step.
+constexpr int kColStages = 4;
+constexpr int kColSlab = 64;
+
+template <class TA, class TC>
+__global__ void __launch_bounds__(128) ttv_columns_kernel(const __grid_constant__ TtvParams P) {
+    using Acc = typename AccOf<TA>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (stop_requested(P.stop)) return;
+    const int64_t K = P.K, I = P.I;
+    Acc *bs = (Acc *)smem_raw;
+    const size_t bbytes = ((size_t)K * sizeof(Acc) + 15) & ~(size_t)15;
+    TA *stages = (TA *)(smem_raw + bbytes);  // kColStages x [kColSlab][32]
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+
+    const int64_t iblocks = (I + 31) / 32;
+    const int64_t o = blockIdx.x / iblocks;
+    const int64_t i0 = (blockIdx.x - o * iblocks) * 32;
+    const int ncol = (int)((I - i0) < 32 ? (I - i0) : 32);
+    const TA *base = (const TA *)P.a + o * K * I + i0;
+    const int nslab = (int)((K + kColSlab - 1) / kColSlab);
+    auto issue = [&](int s) {
+        TA *dst = stages + (s % kColStages) * (kColSlab * 32);
+        const int k0 = s * kColSlab;
+        const int kn = (int)((K - k0) < kColSlab ? (K - k0) : kColSlab);
+        for (int e = threadIdx.x; e < kn * 32; e += blockDim.x) {
+            const int kk = e >> 5, c = e & 31;
+            if (c < ncol) cp_async<sizeof(TA)>(dst + e, base + (int64_t)(k0 + kk) * I + c);
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < kColStages - 1; ++s) {
+        if (s < nslab) issue(s);
+        cp_async_commit();
+    }
+    Acc acc = Acc(0);
+    const int lane = threadIdx.x;
+    for (int s = 0; s < nslab; ++s) {
+        cp_async_wait<kColStages - 2>();
+        __syncthreads();
+        if (s + kColStages - 1 < nslab) issue(s + kColStages - 1);
+        cp_async_commit();
+        if (threadIdx.x < 32) {
+            const TA *st = stages + (s % kColStages) * (kColSlab * 32) + lane;
+            const int k0 = s * kColSlab;
+            const int kn = (int)((K - k0) < kColSlab ? (K - k0) : kColSlab);
+#pragma unroll 8
+            for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)st[kk * 32], bs[k0 + kk]);
         }
     }
-    for (; k < K; ++k) {
-        Acc v[VEC];
-        VecLoad<TA, VEC>::ld(pa + k * I, v);
-        const Acc bk = P.b_smem ? bs[k] : load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[j], bk);
+    cp_async_wait<0>();
+    if (threadIdx.x < ncol) {
+        const int64_t i = i0 + lane;
+        const int64_t off = P.ident ? o * I + i : P.out_map.map((uint32_t)o) + P.in_map.map((uint32_t)i);
+        ((TC *)P.c)[off] = narrow<TC>(acc);
     }
-    store_outputs<TC, VEC>(P, o, i0, acc);
+    if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
 // ------------------------------------------------------------- regime S
@@ -347,6 +415,7 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
         }
     }
     cp_async_wait<0>();
+    if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
 // ------------------------------------------------------------- planning
@@ -466,6 +535,15 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
 
 template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
+    if (L.regime == 2) {
+        auto kern = ttv_columns_kernel<TA, TC>;
+        if (L.smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<L.grid, L.block, L.smem, st>>>(L.P);
+        return cudaGetLastError();
+    }
     if (L.regime == 0) {
         constexpr int U = 8;
         if constexpr (sizeof(TA) == 4) {
@@ -506,7 +584,8 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
 // Entry used by tl_ttv and by the HOPM orchestration (which passes a stop
 // flag and binary64 outputs for float32 storage).
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
-                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st) {
+                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
+                const FusedNorm *fn) {
     Canon cn;
     if (!canon_contraction(a, m0, 0, cn)) {
         set_error("ttv: operand A is not a dense permutation layout (materialise views first)");
@@ -537,7 +616,15 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     if (P.O * P.I == 0) return TL_OK;
     const uintptr_t base = (uintptr_t)P.a;
     bool ok;
-    if (P.I >= 32) {
+    if (P.I >= 32 && P.O * P.I <= 8192 && P.K <= 8192) {
+        // few strided outputs: column blocks keep a whole [K][32] block in flight
+        L.regime = 2;
+        const int64_t iblocks = (P.I + 31) / 32;
+        L.grid = dim3((unsigned)(P.O * iblocks));
+        L.block = dim3(128);
+        L.smem = (((size_t)P.K * 8 + 15) & ~(size_t)15) + (size_t)kColStages * kColSlab * 32 * s;
+        ok = true;
+    } else if (P.I >= 32) {
         ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
     } else {
         ok = plan_staged(L, (int64_t)s, base, di.num_sms);
@@ -546,6 +633,11 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     if (!ok) {
         set_error("ttv: no launch plan");
         return TL_EUNSUPPORTED;
+    }
+    if (fn != nullptr && fn->enabled) {
+        // the last CTA stages w (= this ttv's output) in its shared memory
+        P.fn = *fn;
+        L.smem = std::max(L.smem, (size_t)fn->n * sizeof(double));
     }
     cudaError_t e;
     if (a.dtype == TL_F32 && c_dtype == TL_F32) e = launch_typed<float, float>(L, st);

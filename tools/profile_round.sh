@@ -1,0 +1,15 @@
+#!/bin/bash
+# One GPU session producing the round's evidence under gpurun_out/:
+#   bench line, ncu launch list of the bench command, ncu --set full of the
+#   ttv kernels (regime S + regime B) and the FP64 GETT, clock samples.
+set -u
+mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1
+tail -1 gpurun_out/bench_full.log > gpurun_out/bench_line.json
+CMD="python bench.py --steps 2 --warmup 3 --no-components --no-cpu --no-e2e"
+timeout 300 $CMD > gpurun_out/bench_small.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+    --log-file gpurun_out/launches.csv $CMD > gpurun_out/launches_ncu.log 2>&1
+tools/ncu_box.sh prof_ttv "ttv_" cfg2
+tools/ncu_box.sh prof_ttm "ttm_dmma" cfg3
+du -sh gpurun_out

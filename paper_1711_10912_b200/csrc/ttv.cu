@@ -158,67 +158,118 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
-// ------------------------------------------------------------- column blocks
-// Strided fibers with few outputs (O*I small, e.g. HOPM's 400x400
-// intermediates): one CTA per (o, 32 consecutive i); 128 threads stream
-// k-slabs of the [K][32] column block into shared memory (4-stage cp.async),
-// warp 0 folds its 32 columns in k order.  Latency-bound by design: the
-// whole column block is in flight at once instead of one load per fold step.
-constexpr int kColStages = 4;
-constexpr int kColSlab = 64;
+// ------------------------------------------------------------- small problems
+// Few outputs (e.g. HOPM's 400x400 intermediates, L2-resident): the fold
+// chain of each output (K dependent adds) is the critical path, so each CTA
+// owns 32 outputs, issues the loads of its WHOLE input block up front (one
+// mbarrier per 64-k slab, completed by cp.async.mbarrier.arrive), and warp 0
+// folds slab by slab as they land.  Two block shapes:
+//   COLS (I >= 32): outputs (o, i0..i0+31), element (k, j) at o*K*I + k*I + i0 + j,
+//                   smem [k][32];
+//   ROWS (I == 1):  outputs o0..o0+31, element (k, j) at (o0 + j)*K + k,
+//                   smem [j][pitch] with an odd pitch (conflict-free folds).
+constexpr int kSmallSlab = 64;
+constexpr int kSmallMaxSlabs = 64;  // K <= 4096
 
-template <class TA, class TC>
-__global__ void __launch_bounds__(128) ttv_columns_kernel(const __grid_constant__ TtvParams P) {
+template <class TA, class TC, bool ROWS, bool PAIRS>
+__global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ TtvParams P) {
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[kSmallMaxSlabs];
     if (stop_requested(P.stop)) return;
     const int64_t K = P.K, I = P.I;
+    const int nslab = (int)((K + kSmallSlab - 1) / kSmallSlab);
     Acc *bs = (Acc *)smem_raw;
     const size_t bbytes = ((size_t)K * sizeof(Acc) + 15) & ~(size_t)15;
-    TA *stages = (TA *)(smem_raw + bbytes);  // kColStages x [kColSlab][32]
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+    TA *data = (TA *)(smem_raw + bbytes);
+    // ROWS pitch: odd (scalar LDS), or = 2 mod 4 with 16-byte pairs (LDS.128)
+    const int pitch = PAIRS ? (int)((K + 2) + (((K + 2) / 2) % 2 == 0 ? 2 : 0)) : (int)(K | 1);
 
-    const int64_t iblocks = (I + 31) / 32;
-    const int64_t o = blockIdx.x / iblocks;
-    const int64_t i0 = (blockIdx.x - o * iblocks) * 32;
-    const int ncol = (int)((I - i0) < 32 ? (I - i0) : 32);
-    const TA *base = (const TA *)P.a + o * K * I + i0;
-    const int nslab = (int)((K + kColSlab - 1) / kColSlab);
-    auto issue = [&](int s) {
-        TA *dst = stages + (s % kColStages) * (kColSlab * 32);
-        const int k0 = s * kColSlab;
-        const int kn = (int)((K - k0) < kColSlab ? (K - k0) : kColSlab);
-        for (int e = threadIdx.x; e < kn * 32; e += blockDim.x) {
-            const int kk = e >> 5, c = e & 31;
-            if (c < ncol) cp_async<sizeof(TA)>(dst + e, base + (int64_t)(k0 + kk) * I + c);
-        }
-    };
-#pragma unroll
-    for (int s = 0; s < kColStages - 1; ++s) {
-        if (s < nslab) issue(s);
-        cp_async_commit();
+    int64_t o = 0, i0 = 0, o0 = 0;
+    int nout;
+    const TA *base;
+    if constexpr (ROWS) {
+        o0 = (int64_t)blockIdx.x * 32;
+        nout = (int)((P.O - o0) < 32 ? (P.O - o0) : 32);
+        base = (const TA *)P.a + o0 * K;
+    } else {
+        const int64_t iblocks = (I + 31) / 32;
+        o = blockIdx.x / iblocks;
+        i0 = (blockIdx.x - o * iblocks) * 32;
+        nout = (int)((I - i0) < 32 ? (I - i0) : 32);
+        base = (const TA *)P.a + o * K * I + i0;
     }
-    Acc acc = Acc(0);
-    const int lane = threadIdx.x;
-    for (int s = 0; s < nslab; ++s) {
-        cp_async_wait<kColStages - 2>();
-        __syncthreads();
-        if (s + kColStages - 1 < nslab) issue(s + kColStages - 1);
-        cp_async_commit();
-        if (threadIdx.x < 32) {
-            const TA *st = stages + (s % kColStages) * (kColSlab * 32) + lane;
-            const int k0 = s * kColSlab;
-            const int kn = (int)((K - k0) < kColSlab ? (K - k0) : kColSlab);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nslab; ++s) mbar_init(&bars[s], blockDim.x);
+        mbar_fence_init();
+    }
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+    __syncthreads();
+    if (threadIdx.x >= 32) {
+        // warps 1..3 put the whole block in flight; warp 0 only folds
+        const int t = threadIdx.x - 32, nt = blockDim.x - 32;
+        constexpr int E = PAIRS ? 2 : 1;  // elements per copy
+        for (int s = 0; s < nslab; ++s) {
+            const int k0 = s * kSmallSlab;
+            const int kn = (int)((K - k0) < kSmallSlab ? (K - k0) : kSmallSlab);
+            for (int e = t; e < kSmallSlab * 32 / E; e += nt) {
+                if constexpr (ROWS) {
+                    constexpr int PR = kSmallSlab / E;  // pieces per row slab
+                    const int j = e / PR, kk = (e % PR) * E;  // lanes walk k (contiguous rows)
+                    if (kk < kn && j < nout)
+                        cp_async<E * sizeof(TA)>(data + j * pitch + k0 + kk, base + (int64_t)j * K + k0 + kk);
+                } else {
+                    constexpr int PC = 32 / E;  // pieces per k-row
+                    const int kk = e / PC, j = (e % PC) * E;  // lanes walk i (contiguous columns)
+                    if (kk < kn && j < nout)
+                        cp_async<E * sizeof(TA)>(data + (k0 + kk) * 32 + j, base + (int64_t)(k0 + kk) * I + j);
+                }
+            }
+            cp_async_mbar_arrive(&bars[s]);
+        }
+    } else {
+        const int j = threadIdx.x;
+        Acc acc = Acc(0);
+        for (int s = 0; s < nslab; ++s) cp_async_mbar_arrive(&bars[s]);  // warp 0 issues no copies
+        for (int s = 0; s < nslab; ++s) {
+            mbar_wait_parity(&bars[s], 0);
+            const int k0 = s * kSmallSlab;
+            const int kn = (int)((K - k0) < kSmallSlab ? (K - k0) : kSmallSlab);
+            if constexpr (ROWS) {
+                const TA *row = data + j * pitch + k0;
+                if constexpr (PAIRS) {
+                    int kk = 0;
+#pragma unroll 4
+                    for (; kk + 1 < kn; kk += 2) {
+                        const double2 v = *(const double2 *)(row + kk);
+                        const double2 bv = *(const double2 *)(bs + k0 + kk);
+                        acc = fold_step(acc, (Acc)v.x, bv.x);
+                        acc = fold_step(acc, (Acc)v.y, bv.y);
+                    }
+                    if (kk < kn) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
+                } else {
 #pragma unroll 8
-            for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)st[kk * 32], bs[k0 + kk]);
+                    for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
+                }
+            } else {
+                const TA *col = data + k0 * 32 + j;
+#pragma unroll 8
+                for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)col[kk * 32], bs[k0 + kk]);
+            }
+        }
+        if (j < nout) {
+            int64_t off;
+            if constexpr (ROWS) {
+                const int64_t oo = o0 + j;
+                off = P.ident ? oo : P.out_map.map((uint32_t)oo);
+            } else {
+                const int64_t i = i0 + j;
+                off = P.ident ? o * I + i : P.out_map.map((uint32_t)o) + P.in_map.map((uint32_t)i);
+            }
+            ((TC *)P.c)[off] = narrow<TC>(acc);
         }
     }
     cp_async_wait<0>();
-    if (threadIdx.x < ncol) {
-        const int64_t i = i0 + lane;
-        const int64_t off = P.ident ? o * I + i : P.out_map.map((uint32_t)o) + P.in_map.map((uint32_t)i);
-        ((TC *)P.c)[off] = narrow<TC>(acc);
-    }
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
@@ -535,8 +586,11 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
 
 template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
-    if (L.regime == 2) {
-        auto kern = ttv_columns_kernel<TA, TC>;
+    if (L.regime == 2 || L.regime == 3) {
+        auto kern = (L.regime == 3) ? ttv_small_kernel<TA, TC, true, false> : ttv_small_kernel<TA, TC, false, false>;
+        if constexpr (sizeof(TA) == 8 && std::is_same<typename AccOf<TA>::type, double>::value) {
+            if (L.vec == 2) kern = (L.regime == 3) ? ttv_small_kernel<TA, TC, true, true> : ttv_small_kernel<TA, TC, false, true>;
+        }
         if (L.smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
             if (e != cudaSuccess) return e;
@@ -616,13 +670,20 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     if (P.O * P.I == 0) return TL_OK;
     const uintptr_t base = (uintptr_t)P.a;
     bool ok;
-    if (P.I >= 32 && P.O * P.I <= 8192 && P.K <= 8192) {
-        // few strided outputs: column blocks keep a whole [K][32] block in flight
-        L.regime = 2;
-        const int64_t iblocks = (P.I + 31) / 32;
-        L.grid = dim3((unsigned)(P.O * iblocks));
+    const size_t small_bbytes = ((size_t)P.K * 8 + 15) & ~(size_t)15;
+    const bool small_cols = P.I >= 32 && P.O * P.I <= 8192;
+    const bool small_rows = P.I == 1 && P.O <= 8192;
+    if ((small_cols || small_rows) && P.K <= kSmallSlab * kSmallMaxSlabs &&
+        small_bbytes + 32 * (size_t)(P.K | 1) * s <= 200 * 1024) {
+        // few outputs: whole 32-output input blocks in flight, one fold warp
+        L.regime = small_rows ? 3 : 2;
+        L.grid = dim3((unsigned)(small_rows ? (P.O + 31) / 32 : P.O * ((P.I + 31) / 32)));
         L.block = dim3(128);
-        L.smem = (((size_t)P.K * 8 + 15) & ~(size_t)15) + (size_t)kColStages * kColSlab * 32 * s;
+        // 16-byte element pairs for float64 when every pair is aligned and in range
+        const bool pairs = (a.dtype == TL_F64) && (base % 16 == 0) && (small_rows ? (P.K % 2 == 0) : (P.I % 2 == 0));
+        L.vec = pairs ? 2 : 1;
+        const int64_t pitch = pairs ? (P.K + 2) + (((P.K + 2) / 2) % 2 == 0 ? 2 : 0) : (P.K | 1);
+        L.smem = small_bbytes + 32 * (size_t)std::max<int64_t>(pitch, P.K) * s;
         ok = true;
     } else if (P.I >= 32) {
         ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);

@@ -1,0 +1,356 @@
+"""GPU coverage beyond the golden fixtures: edge shapes for every kernel
+regime, all ttm paths, the container API (relayout/assign/equality/
+interchange), error behaviour, allocation discipline, CUDA-graph capture,
+and full-size config-3 ttm checked on sampled outputs."""
+
+import math
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def tl():
+    import paper_1711_10912_b200 as m
+
+    return m
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype.itemsize == 8 else np.uint32)
+
+
+def dev(buf, shape, layout, dtype=None):
+    return tl().DenseTensor.from_memory(tuple(shape), np.asarray(buf), layout=tuple(layout), dtype=dtype)
+
+
+def check_ttv(T, layout, mode, b, dtype):
+    shape = T.shape
+    buf = W.layout_buffer(T, layout)
+    C = tl().ttv(dev(buf, shape, layout), tl().DenseTensor.from_memory((shape[mode - 1],), b), mode)
+    want = O.ttv(buf, shape, W.compute_strides(shape, layout), b, mode)
+    if dtype == "float32":
+        want = want.astype(np.float32)
+    assert np.array_equal(bits(C.numpy()), bits(want)), (shape, layout, mode)
+
+
+@pytest.mark.parametrize("case", [
+    ((1, 5, 7), (1, 2, 3), 1),            # K = 1
+    ((6, 1, 9), (2, 3, 1), 2),            # K = 1, permuted
+    ((5, 1, 1, 8), (3, 1, 4, 2), 4),      # extent-1 free dims
+    ((2, 2, 2, 2, 2, 2, 2, 2, 2, 2), tuple(range(10, 0, -1)), 5),   # order 10
+    ((2,) * 16, tuple(range(16, 0, -1)), 9),                          # order 16 (max)
+    ((3, 9000), (1, 2), 2),               # K > smem vector limit, I = 3
+    ((9000, 3), (2, 1), 1),               # K large, contracted stride 1 with slabs
+    ((33, 5, 127), (3, 1, 2), 3),         # odd K, stride-1 contraction
+    ((64, 48, 9), (3, 1, 2), 3),          # K = 9 regime S
+    ((400, 400), (1, 2), 1),              # small-problem rows kernel
+    ((400, 400), (1, 2), 2),              # small-problem column kernel
+    ((37, 33, 40), (2, 3, 1), 2),         # regime B, permuted output
+])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_ttv_edge_shapes_bit_exact(gpu, case, dtype):
+    shape, layout, mode = case
+    rng = np.random.default_rng(hash((shape, layout, mode)) % 2**32)
+    T = rng.uniform(-1, 1, size=shape).astype(dtype)
+    b = rng.uniform(-1, 1, size=shape[mode - 1]).astype(dtype)
+    check_ttv(T, layout, mode, b, dtype)
+
+
+def test_ttv_float32_tensor_float64_vector(gpu):
+    rng = np.random.default_rng(11)
+    T = rng.uniform(-1, 1, size=(20, 30, 40)).astype(np.float32)
+    b = rng.uniform(-1, 1, size=30)  # float64 vector
+    for layout in ((1, 2, 3), (3, 2, 1)):
+        buf = W.layout_buffer(T, layout)
+        C = tl().ttv(dev(buf, T.shape, layout), tl().DenseTensor.from_memory((30,), b), 2)
+        want = O.ttv(buf.astype(np.float64), T.shape, W.compute_strides(T.shape, layout), b, 2)
+        assert np.array_equal(bits(C.numpy()), bits(want.astype(np.float32)))
+
+
+def ttm_case(shape, layout, mode, J, blayout, dtype, seed):
+    rng = np.random.default_rng(seed)
+    if dtype == "int64":
+        T = rng.integers(-20, 20, size=shape)
+        M = rng.integers(-20, 20, size=(J, shape[mode - 1]))
+    else:
+        T = rng.standard_normal(shape).astype(dtype)
+        M = rng.standard_normal((J, shape[mode - 1])).astype(dtype)
+    buf, mbuf = W.layout_buffer(T, layout), W.layout_buffer(M, blayout)
+    C = tl().ttm(dev(buf, shape, layout), dev(mbuf, M.shape, blayout), mode)
+    st = W.compute_strides(shape, layout)
+    bst = W.compute_strides(M.shape, blayout)
+    want = O.ttm(buf, shape, st, mbuf, M.shape, bst, mode)
+    return C.numpy(), want, (buf, shape, st, mbuf, M.shape, bst)
+
+
+@pytest.mark.parametrize("case", [
+    ((48, 40, 36), (1, 2, 3), 1, 64, (1, 2)),   # GETT, K-major A
+    ((48, 40, 36), (1, 2, 3), 2, 64, (2, 1)),   # GETT, N-major A
+    ((48, 40, 36), (3, 2, 1), 2, 96, (1, 2)),   # GETT, 2-D tile (C-fast != A-fast)
+    ((48, 40, 36), (3, 2, 1), 3, 33, (2, 1)),   # GETT, odd J
+    ((30, 29, 31), (2, 3, 1), 1, 40, (1, 2)),   # GETT, odd extents (8-byte loads)
+    ((3, 33, 5, 17), (1, 2, 3, 4), 2, 16, (1, 2)),  # staged DMMA (J = 16)
+    ((12, 40, 10), (2, 3, 1), 2, 24, (2, 1)),   # staged DMMA (J = 24: two m-tiles)
+    ((7, 9, 11), (3, 1, 2), 3, 5, (1, 2)),      # tiny J
+    ((64, 8, 64), (1, 2, 3), 2, 200, (1, 2)),   # K < 16 -> exact fold path
+])
+def test_ttm_float64_paths(gpu, case):
+    shape, layout, mode, J, blayout = case
+    got, want, (buf, shape, st, mbuf, mshape, bst) = ttm_case(shape, layout, mode, J, blayout, "float64", 5)
+    bound = O.ttm(np.abs(buf), shape, st, np.abs(mbuf), mshape, bst, mode)
+    assert np.all(np.abs(got - want) <= 1e-12 * bound)
+
+
+@pytest.mark.parametrize("dtype", ["int64", "float32"])
+def test_ttm_exact_dtypes(gpu, dtype):
+    for case in [((9, 7, 5), (2, 1, 3), 2, 6, (2, 1)), ((40, 30, 20), (1, 2, 3), 1, 48, (1, 2)),
+                 ((5, 6, 7, 8), (4, 3, 2, 1), 3, 3, (1, 2))]:
+        shape, layout, mode, J, blayout = case
+        got, want, _ = ttm_case(shape, layout, mode, J, blayout, dtype, 6)
+        if dtype == "float32":
+            want = want.astype(np.float32)  # binary64 products of float32 values are exact
+        assert np.array_equal(bits(got), bits(want)), case
+
+
+@pytest.mark.parametrize("q,layout", [(1, (1, 2, 3)), (2, (1, 2, 3)), (3, (1, 2, 3)),
+                                      (1, (3, 2, 1)), (2, (3, 2, 1)), (3, (3, 2, 1))])
+def test_cfg3_ttm_full_size_sampled(gpu, q, layout):
+    """Config 3 at full size: 4096 sampled outputs vs the oracle's k-order fold,
+    plus linearity in B, within 1e-12 of sum|A||B|."""
+    A_, B_ = W.cfg3()
+    buf = W.layout_buffer(A_, layout)
+    st = W.compute_strides(A_.shape, layout)
+    mbuf = W.layout_buffer(B_, (1, 2))
+    A = dev(buf, A_.shape, layout)
+    Bm = dev(mbuf, B_.shape, (1, 2))
+    C = tl().ttm(A, Bm, q).numpy()
+    sel = np.random.default_rng(q).integers(0, C.size, size=4096)
+    want = O.ttm(buf, A_.shape, st, mbuf, B_.shape, (1, 384), q, select=sel)
+    bound = O.ttm(np.abs(buf), A_.shape, st, np.abs(mbuf), B_.shape, (1, 384), q, select=sel)
+    assert np.all(np.abs(C[sel] - want) <= 1e-12 * bound)
+    # linearity: ttm(A, 2B) == 2 ttm(A, B) exactly (scaling by 2 is exact)
+    C2 = tl().ttm(A, dev(2.0 * mbuf, B_.shape, (1, 2)), q).numpy()
+    assert np.array_equal(C2, 2.0 * C)
+
+
+def test_inner_norm_layout_mix(gpu):
+    rng = np.random.default_rng(3)
+    shape = (33, 20, 17, 6)
+    for dtype in ("float64", "float32", "int64"):
+        if dtype == "int64":
+            Ta, Tb = rng.integers(-9, 9, size=shape), rng.integers(-9, 9, size=shape)
+        else:
+            Ta, Tb = rng.uniform(-1, 1, size=shape).astype(dtype), rng.uniform(-1, 1, size=shape).astype(dtype)
+        for la, lb in [((1, 2, 3, 4), (1, 2, 3, 4)), ((1, 2, 3, 4), (4, 3, 2, 1)), ((2, 4, 1, 3), (3, 1, 4, 2)),
+                       ((1, 3, 2, 4), (1, 4, 3, 2))]:
+            A, B = dev(W.layout_buffer(Ta, la), shape, la), dev(W.layout_buffer(Tb, lb), shape, lb)
+            got = tl().inner_product_tensors(A, B)
+            want = O.inner(W.layout_buffer(Ta, la), shape, W.compute_strides(shape, la), W.layout_buffer(Tb, lb),
+                           W.compute_strides(shape, lb))
+            if dtype == "int64":
+                assert got == want
+            else:
+                bound = float(np.sum(np.abs(Ta.astype(np.float64)) * np.abs(Tb.astype(np.float64))))
+                assert abs(got - want) <= 1e-12 * bound
+        if dtype != "int64":
+            A = dev(W.layout_buffer(Ta, (3, 1, 4, 2)), shape, (3, 1, 4, 2))
+            n = tl().frobenius_norm(A)
+            assert abs(n - O.norm(W.layout_buffer(Ta, (3, 1, 4, 2)), shape,
+                                  W.compute_strides(shape, (3, 1, 4, 2)))) <= 1e-12 * n
+    assert tl().inner_product_flat(dev(np.ones(8), (2, 2, 2), (1, 2, 3)), dev(np.ones(8), (2, 2, 2), (3, 2, 1)),
+                                   init=1.5) == 9.5
+
+
+def test_times_vectors_and_matrices(gpu):
+    rng = np.random.default_rng(4)
+    shape, layout = (7, 6, 5, 4), (2, 4, 1, 3)
+    T = rng.standard_normal(shape)
+    A = dev(W.layout_buffer(T, layout), shape, layout)
+    vs = [rng.standard_normal(n) for n in shape]
+    V = [tl().DenseTensor.from_memory((n,), v) for n, v in zip(shape, vs)]
+    # full contraction -> shape (1,), the reference's fold order (highest mode first)
+    full = tl().times_vectors(A, V, [1, 2, 3, 4])
+    cur = T
+    for m in (4, 3, 2):
+        cur_shape = cur.shape
+        cur = O.ttv(cur.ravel("F"), cur_shape, W.compute_strides(cur_shape, W.first_order(len(cur_shape))),
+                    vs[m - 1], m).reshape([s for i, s in enumerate(cur_shape) if i != m - 1], order="F")
+    want = O.inner(cur.ravel("F"), cur.shape, (1,), vs[0], (1,))
+    assert full.shape == (1,) and full.item() == want
+    # times_matrices == chained ttm, highest mode first
+    Ms = [rng.standard_normal((3, shape[0])), rng.standard_normal((2, shape[2]))]
+    Bm = [tl().DenseTensor.from_memory(M.shape, M.ravel("F")) for M in Ms]
+    got = tl().times_matrices(A, Bm, [1, 3])
+    ref = tl().ttm(tl().ttm(A, Bm[1], 3), Bm[0], 1)
+    assert tl().tensors_equal(got, ref)
+    with pytest.raises(ValueError):
+        tl().times_vectors(A, V[:2], [2, 1])
+    with pytest.raises(ValueError):
+        tl().times_vectors(A, V, modes=[1, 2, 3, 4], skip=1)
+
+
+@pytest.mark.parametrize("shape", [(5, 7), (4, 6, 5), (3, 4, 5, 2), (6, 5, 4, 3, 2), (9,)])
+def test_hopm_random_layouts_bit_exact(gpu, shape):
+    rng = np.random.default_rng(len(shape))
+    p = len(shape)
+    for seed in range(3):
+        layout = W.random_layout(p, seed)
+        T = rng.uniform(-1, 1, size=shape)
+        buf = W.layout_buffer(T, layout)
+        st = tl().hopm(dev(buf, shape, layout), max_sweeps=15, tol=0.0)
+        ref = O.hopm(buf, shape, W.compute_strides(shape, layout), max_sweeps=15, tol=0.0)
+        assert st.lambda_history == ref["lambda_history"]
+        assert st.l == ref["l"]
+        for u, r in zip(st.u, ref["u"]):
+            assert np.array_equal(bits(u.numpy()), bits(r))
+    # float32 storage: the reference computes on the float32 values in binary64
+    T = rng.uniform(-1, 1, size=shape).astype(np.float32)
+    buf = W.layout_buffer(T, W.first_order(p))
+    st = tl().hopm(dev(buf, shape, W.first_order(p)), max_sweeps=6, tol=0.0)
+    ref = O.hopm(buf.astype(np.float64), shape, W.compute_strides(shape, W.first_order(p)), max_sweeps=6, tol=0.0)
+    assert st.lambda_history == ref["lambda_history"]
+
+
+def test_hopm_convergence_and_errors(gpu):
+    m = tl()
+    rng = np.random.default_rng(9)
+    us = [rng.standard_normal(n) for n in (6, 5, 4)]
+    us = [u / np.linalg.norm(u) for u in us]
+    T = 3.0 * np.einsum("i,j,k->ijk", *us)
+    A = dev(T.ravel("F"), T.shape, (1, 2, 3))
+    st = m.hopm(A, max_sweeps=50, tol=1e-10)
+    ref = O.hopm(T.ravel("F"), T.shape, (1, 6, 30), max_sweeps=50, tol=1e-10)
+    assert st.converged and st.sweeps == ref["sweeps"] < 50
+    assert st.lambda_history == ref["lambda_history"] and abs(st.scale - 3.0) < 1e-10
+    st1 = m.hopm(A, max_sweeps=1)
+    assert st1.sweeps == 1 and not st1.converged
+    with pytest.raises(ValueError):
+        m.hopm(A, max_sweeps=0)
+    with pytest.raises(ValueError):
+        m.hopm(A, u0=[m.DenseTensor((6,), fill_value=1.0)])
+    with pytest.raises(ValueError):
+        m.hopm(A, u0=[m.DenseTensor((6,)), m.DenseTensor((5,), fill_value=1.0), m.DenseTensor((4,), fill_value=1.0)])
+    with pytest.raises(m.DegenerateInputError):
+        m.hopm(m.DenseTensor((3, 4, 2)))
+    # a runner replays the captured graph with identical results
+    r = m.HopmRunner(A, max_sweeps=5, tol=0.0)
+    a1 = r.run().lambda_history
+    a2 = r.run().lambda_history
+    r.close()
+    assert a1 == a2
+
+
+def test_container_api(gpu):
+    m = tl()
+    t = m.DenseTensor((2, 3), offsets=(1, -1), layout=(2, 1))
+    assert t.strides == (3, 1) and t.dtype == torch.float64 and t.data == [0.0] * 6
+    t[1, -1] = 5.0
+    t[2, 1] = 7.0
+    assert t[1, -1] == 5.0 and t.get_memory(0) == 5.0 and t.get_memory(5) == 7.0
+    with pytest.raises(IndexError):
+        t[0, 0]
+    with pytest.raises(ValueError):
+        t[1]
+    u = m.DenseTensor.from_memory((2, 3), [1, 2, 3, 4, 5, 6])
+    assert u.dtype == torch.int64
+    assert m.DenseTensor.from_memory((2,), [1.0, 2]).dtype == torch.float64
+    assert m.DenseTensor.from_memory((2,), np.ones(2, dtype=np.float32)).dtype == torch.float32
+    with pytest.raises(ValueError):
+        m.DenseTensor.from_memory((2, 2), [1, 2, 3])
+    # relayout keeps index -> value, bit for bit
+    rng = np.random.default_rng(1)
+    T = rng.standard_normal((5, 4, 3, 6))
+    A = dev(W.layout_buffer(T, (1, 2, 3, 4)), T.shape, (1, 2, 3, 4))
+    B = A.copy()
+    B.relayout((3, 1, 4, 2))
+    assert np.array_equal(B.numpy(), W.layout_buffer(T, (3, 1, 4, 2)))
+    assert m.tensors_equal(A, B) and A == B
+    C = m.DenseTensor((5, 4, 3, 6), layout=(4, 3, 2, 1))
+    C.assign(A)
+    assert C.layout == (4, 3, 2, 1) and np.array_equal(C.numpy(), W.layout_buffer(T, (4, 3, 2, 1)))
+    D = m.DenseTensor.from_dict(A.to_dict())
+    assert D == A
+    B.set_memory(0, 99.0)
+    assert not m.tensors_equal(A, B)
+    A.reshape((20, 18))
+    assert A.shape == (20, 18) and A.layout == (1, 2)
+    with pytest.raises(ValueError):
+        A.reshape((7, 7))
+
+
+def test_errors_mirror_reference(gpu):
+    m = tl()
+    a = m.DenseTensor((3, 4))
+    with pytest.raises(ValueError):
+        m.ttv(a, m.DenseTensor((4,)), 3)
+    with pytest.raises(ValueError):
+        m.ttv(a, m.DenseTensor((5,)), 2)
+    with pytest.raises(ValueError):
+        m.ttv(m.DenseTensor((4,)), m.DenseTensor((4,)), 1)
+    with pytest.raises(ValueError):
+        m.ttm(a, m.DenseTensor((2, 5)), 2)
+    with pytest.raises(ValueError):
+        m.ttm(a, m.DenseTensor((2, 4, 1)), 2)
+    with pytest.raises(ValueError):
+        m.inner_product_tensors(m.DenseTensor((2, 3)), m.DenseTensor((3, 2)))
+    # column vectors are accepted (contraction.py:58-69)
+    rng = np.random.default_rng(0)
+    x = dev(rng.standard_normal(12), (3, 4), (2, 1))
+    col = m.DenseTensor.from_memory((4, 1), [1.0, 2.0, 3.0, 4.0])
+    flat = m.DenseTensor.from_memory((4,), [1.0, 2.0, 3.0, 4.0])
+    assert m.tensors_equal(m.ttv(x, col, 2), m.ttv(x, flat, 2))
+
+
+def test_allocation_discipline(gpu, monkeypatch):
+    """ttv/ttm allocate exactly one DenseTensor (test_contraction.py:398-425)."""
+    m = tl()
+    a = dev(np.arange(24.0), (3, 4, 2), (2, 3, 1))
+    b = m.DenseTensor.from_memory((4,), [1.0, 2.0, 3.0, 4.0])
+    mat = m.DenseTensor.from_memory((5, 4), np.arange(20.0))
+    counter = [0]
+    original = m.DenseTensor.__init__
+
+    def counting(self, *args, **kw):
+        counter[0] += 1
+        return original(self, *args, **kw)
+
+    monkeypatch.setattr(m.DenseTensor, "__init__", counting)
+    m.ttv(a, b, 2)
+    assert counter[0] == 1
+    counter[0] = 0
+    m.ttm(a, mat, 2)
+    assert counter[0] == 1
+
+
+def test_cuda_graph_capture(gpu):
+    """The ABI calls are capturable: a graph of ttv + ttm + norm replays
+    to the same bits as eager execution."""
+    m = tl()
+    import paper_1711_10912_b200.contraction as C
+
+    rng = np.random.default_rng(2)
+    T = rng.standard_normal((40, 50, 60))
+    A = dev(W.layout_buffer(T, (2, 3, 1)), T.shape, (2, 3, 1))
+    v = m.DenseTensor.from_memory((50,), rng.standard_normal(50))
+    M = m.DenseTensor.from_memory((64, 60), rng.standard_normal(64 * 60))
+    eager = (m.ttv(A, v, 2).numpy(), m.ttm(A, M, 3).numpy(), C.frobenius_norm_device(A).item())
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        m.ttv(A, v, 2), m.ttm(A, M, 3), C.frobenius_norm_device(A)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        o1, o2, o3 = m.ttv(A, v, 2), m.ttm(A, M, 3), C.frobenius_norm_device(A)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(o1.numpy(), eager[0]) and np.array_equal(o2.numpy(), eager[1]) and o3.item() == eager[2]

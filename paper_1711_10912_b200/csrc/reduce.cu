@@ -23,6 +23,7 @@
 // The last CTA to finish (atomic ticket) combines the per-CTA partials and
 // resets the ticket, so the workspace stays zeroed for graph replay.
 #include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <type_traits>
 #include <vector>
@@ -306,6 +307,67 @@ __global__ void __launch_bounds__(256) dot_tiled_kernel(const __grid_constant__ 
     finish(P, acc);
 }
 
+// ------------------------------------------------------------ dot_tiled (vector)
+// Same contraction with 64x64 tiles and 16-byte loads: a is read along X
+// (its unit-stride dimension) and b along Y, each thread keeps 4 + 4 vectors
+// in flight; b's tile is transposed through shared memory so that a thread
+// multiplies a 16-byte run of a with a 16-byte run of the transposed b tile.
+constexpr int kT = 64;
+
+template <class T>
+__global__ void __launch_bounds__(256) dot_tiled_vec_kernel(const __grid_constant__ ReduceParams P) {
+    using Acc = typename RedAcc<T>::type;
+    constexpr int V = 16 / sizeof(T);     // elements per 16-byte vector
+    constexpr int VR = kT / V;            // vectors per tile row
+    constexpr int PITCH = kT;             // bt[y][x ^ swz(y)]: XOR swizzle in units of V
+    __shared__ __align__(16) T bt[kT * PITCH];
+    auto swz = [](int y) { return ((y / V) & 7) * V; };
+    ThreadAcc<T> ta;
+    ta.zero();
+    const T *a = (const T *)P.a;
+    const T *b = (const T *)P.b;
+    const int64_t per_rest = P.tiles_x * P.tiles_y;
+    const int64_t tiles = per_rest * P.n_rest;
+    constexpr int NV = kT * VR / 256;  // vectors per thread per operand tile
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t rest = t / per_rest;
+        const int64_t txy = t - rest * per_rest;
+        const int64_t ty = txy / P.tiles_x;
+        const int64_t tx = txy - ty * P.tiles_x;
+        const int64_t x0 = tx * kT, y0 = ty * kT;
+        const int64_t ra = P.rest_a.map((uint32_t)rest), rb = P.rest_b.map((uint32_t)rest);
+        T av[NV][V], bv[NV][V];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int row = e / VR, vc = (e % VR) * V;
+            // b: row = x (fixed), along y; a: row = y (fixed), along x
+            *(uint4 *)bv[q] = __ldcs((const uint4 *)(b + rb + (x0 + row) * P.b_sX + y0 + vc));
+            *(uint4 *)av[q] = __ldcs((const uint4 *)(a + ra + (y0 + row) * P.a_sY + x0 + vc));
+        }
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int row = e / VR, vc = (e % VR) * V;
+#pragma unroll
+            for (int c = 0; c < V; ++c) bt[(vc + c) * PITCH + (row ^ swz(vc + c))] = bv[q][c];  // b(x=row, y)
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int row = e / VR, vc = (e % VR) * V;  // a's row y = row, x = vc..vc+V-1
+            T bb[V];
+            *(uint4 *)bb = *(const uint4 *)(bt + row * PITCH + (vc ^ swz(row)));
+#pragma unroll
+            for (int c = 0; c < V; ++c) ta.add(c, as_acc(av[q][c]), as_acc(bb[c]));
+        }
+        __syncthreads();
+    }
+    Acc acc = block_reduce(ta.total());
+    finish(P, acc);
+}
+
 // ------------------------------------------------------------ planning
 size_t reduce_workspace_bytes() { return (size_t)kMaxPartials * 2 * sizeof(double) + 256; }
 
@@ -371,7 +433,11 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         if (!build_map(rb, P.rows_b)) return TL_EUNSUPPORTED;
         // persistent grid: 4 CTAs per SM, each thread keeps 4 x 16 B in flight
         const int64_t work = (P.n_rows == 1) ? N / 16 : N / 4;
-        int64_t grid = std::min<int64_t>((int64_t)di.num_sms * 4, (work + threads - 1) / threads);
+        static const int64_t ctas_per_sm = [] {
+            const char *ev = getenv("TL_REDUCE_CTAS_PER_SM");
+            return (int64_t)(ev ? atoi(ev) : 4);
+        }();
+        int64_t grid = std::min<int64_t>((int64_t)di.num_sms * ctas_per_sm, (work + threads - 1) / threads);
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, kMaxPartials));
         const uintptr_t pa = (uintptr_t)P.a, pb = (uintptr_t)P.b;
         const bool same = (P.a == P.b) && (a.dtype == b.dtype) && P.n_rows == 1;
@@ -421,6 +487,26 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         P.n_rest = 1;
         for (auto &dg : ma) P.n_rest *= dg.first;
         if (!build_map(ma, P.rest_a) || !build_map(mb, P.rest_b) || P.n_rest > 0xffffffffll) return TL_EUNSUPPORTED;
+        // 64x64 tiles with 16-byte vectors when every tile row is a whole,
+        // aligned run of vectors in both operands
+        if (a.dtype == b.dtype && (a.dtype == TL_F32 || a.dtype == TL_F64)) {
+            const int64_t V = 16 / (int64_t)sa;
+            bool vec = P.nX % kT == 0 && P.nY % kT == 0 && P.a_sY % V == 0 && P.b_sX % V == 0 &&
+                       (uintptr_t)P.a % 16 == 0 && (uintptr_t)P.b % 16 == 0;
+            for (auto &dg : ma) vec = vec && dg.second % V == 0;
+            for (auto &dg : mb) vec = vec && dg.second % V == 0;
+            if (vec) {
+                P.tiles_x = P.nX / kT;
+                P.tiles_y = P.nY / kT;
+                const int64_t tiles = P.tiles_x * P.tiles_y * P.n_rest;
+                const int64_t grid = std::min<int64_t>(std::min<int64_t>((int64_t)di.num_sms * 4, tiles), kMaxPartials);
+                if (a.dtype == TL_F32)
+                    dot_tiled_vec_kernel<float><<<(unsigned)grid, 256, 0, st>>>(P);
+                else
+                    dot_tiled_vec_kernel<double><<<(unsigned)grid, 256, 0, st>>>(P);
+                return cuda_status(cudaGetLastError(), "inner (tiled) launch");
+            }
+        }
         P.tiles_x = (P.nX + 31) / 32;
         P.tiles_y = (P.nY + 31) / 32;
         const int64_t tiles = P.tiles_x * P.tiles_y * P.n_rest;

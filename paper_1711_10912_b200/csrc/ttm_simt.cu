@@ -61,6 +61,9 @@ __global__ void __launch_bounds__(256) ttm_simt_kernel(const __grid_constant__ T
 
 // ------------------------------------------------------------ staged (small J)
 constexpr int kTtmStages = 3;
+// DMMA path: write fragments straight to first-order C (sector-complete per
+// CTA) instead of staging the output tile in shared memory
+constexpr bool kDirectStore = true;
 constexpr int kJB = 16;
 
 template <class T> __device__ __forceinline__ typename AccOf<T>::type mac(typename AccOf<T>::type acc, T a, typename AccOf<T>::type b);
@@ -91,6 +94,13 @@ __device__ __forceinline__ void mma_16x8x4_s(double (&d)[4], double a0, double a
     asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
                  : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
                  : "d"(a0), "d"(a1), "d"(b));
+}
+
+// Output store for layouts whose first-order C is not the tile's contiguous
+// range (kept out of line: it would otherwise be inlined per fragment value).
+template <class T>
+__device__ __noinline__ void store_permuted(const TtmSimtParams &P, int64_t o, uint32_t i, int64_t j, T v) {
+    ((T *)P.c)[P.out_map.map((uint32_t)o) + j * P.jstride + P.in_map.map(i)] = v;
 }
 
 // MT = 0: SIMT fold; MT = 1, 2: FP64 DMMA with MT m16 tiles (J <= 16 MT)
@@ -165,11 +175,10 @@ __global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__
         const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
         auto put = [&](uint32_t r, uint32_t i, int64_t j, Acc v) {
             if (r >= rows || j >= J) return;
-            if (P.ident) {
+            if (P.ident)
                 outs[((size_t)r * J + j) * I + i] = narrow<T>(v);
-            } else {
-                ((T *)P.c)[P.out_map.map((uint32_t)(o0 + r)) + j * P.jstride + P.in_map.map(i)] = narrow<T>(v);
-            }
+            else
+                store_permuted<T>(P, o0 + r, i, j, narrow<T>(v));
         };
         if constexpr (DMMA) {
             // warp w takes groups of 32 positions (4 n8 tiles); all J rows
@@ -211,18 +220,29 @@ __global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__
                         for (int nt = 0; nt < NT; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
                     }
                 }
+                // epilogue: each lane owns columns 2t, 2t+1 of every n8 tile
+                const int Ji = (int)J, Ii = (int)I, rowsi = (int)rows;
 #pragma unroll
-                for (int mm = 0; mm < MT; ++mm) {
+                for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
+                    for (int v = 0; v < 2; ++v) {
+                        const uint32_t pos = p0 + nt * 8 + 2 * t + v;
+                        uint32_t r, i;
+                        P.I_div.divmod(pos, r, i);
+                        if (pos >= slots || (int)r >= rowsi) continue;
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            const uint32_t pos = p0 + nt * 8 + 2 * t + (v & 1);
-                            const int64_t j = mm * 16 + g + 8 * (v >> 1);
-                            if (pos < slots) {
-                                uint32_t r, i;
-                                P.I_div.divmod(pos, r, i);
-                                put(r, i, j, (Acc)acc[mm][nt][v]);
+                        for (int mm = 0; mm < MT; ++mm) {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int j = mm * 16 + g + 8 * h;
+                                if (j >= Ji) continue;
+                                if (P.ident && kDirectStore)
+                                    ((T *)P.c)[o0 * J * I + ((int)r * Ji + j) * Ii + (int)i] =
+                                        narrow<T>((Acc)acc[mm][nt][2 * h + v]);
+                                else if (P.ident)
+                                    outs[((int)r * Ji + j) * Ii + (int)i] = narrow<T>((Acc)acc[mm][nt][2 * h + v]);
+                                else
+                                    put(r, i, j, (Acc)acc[mm][nt][2 * h + v]);
                             }
                         }
                     }
@@ -253,12 +273,19 @@ __global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__
                 }
             }
         }
-        if (P.ident) {
+        if (P.ident && !(DMMA && kDirectStore)) {
             __syncthreads();
             // the tile's outputs are one contiguous range of first-order C
             T *dst = (T *)P.c + o0 * J * I;
-            const int64_t n = rows * J * I;
-            for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = outs[e];
+            const int n = (int)(rows * J * I);
+            constexpr int VE = 16 / sizeof(T);
+            if (((uintptr_t)dst & 15) == 0 && n % VE == 0) {
+                const uint4 *src4 = (const uint4 *)outs;
+                uint4 *dst4 = (uint4 *)dst;
+                for (int e = threadIdx.x; e < n / VE; e += blockDim.x) dst4[e] = src4[e];
+            } else {
+                for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = outs[e];
+            }
         }
     }
     cp_async_wait<0>();

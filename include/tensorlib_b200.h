@@ -108,24 +108,24 @@ int tl_frobenius_norm(const tl_desc *a, const void *a_ptr, double *result_dev,
  * degenerate_sweep, degenerate_mode} (degenerate_* = 0 unless a mode
  * update had norm 0, hopm.py:107-108).  u0_ptrs: NULL (u_ptrs hold the
  * start vectors) or p device vectors copied into u_ptrs at the start of the
- * run, which makes a captured graph replayable.  Every step is the reference's
- * arithmetic (ttv folds, sequential norms, IEEE division), so results are
- * bit-identical to the reference.  a: float64 or float32 storage. */
+ * run, which makes a captured graph replayable.  resid_dev: NULL, or
+ * [max_sweeps] doubles receiving residual(a, state) after every sweep
+ * (track_residuals, hopm.py:114-115).  Every step is the reference's
+ * arithmetic (ttv folds, sequential norms, IEEE division), so lambda and the
+ * vectors are bit-identical to the reference.  a: float64 or float32. */
 int tl_hopm_workspace_bytes(const tl_desc *a, size_t *ws_bytes);
 int tl_hopm(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs, double *const *u_ptrs,
-            int32_t max_sweeps,
-            double tol, double *l_dev, double *hist_dev, int32_t *info_dev, void *ws,
-            size_t ws_bytes, void *stream);
+            int32_t max_sweeps, double tol, double *l_dev, double *hist_dev, int32_t *info_dev,
+            double *resid_dev, void *ws, size_t ws_bytes, void *stream);
 
 /* The same HOPM run captured once into an executable CUDA graph (no host
  * round trip per sweep); launch it with tl_graph_launch.  Pointers and
  * shapes are baked in. */
 typedef struct tl_graph_s *tl_graph;
 int tl_hopm_graph_create(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs,
-                         double *const *u_ptrs,
-                         int32_t max_sweeps, double tol, double *l_dev, double *hist_dev,
-                         int32_t *info_dev, void *ws, size_t ws_bytes, void *stream,
-                         tl_graph *out);
+                         double *const *u_ptrs, int32_t max_sweeps, double tol, double *l_dev,
+                         double *hist_dev, int32_t *info_dev, double *resid_dev, void *ws,
+                         size_t ws_bytes, void *stream, tl_graph *out);
 int tl_graph_launch(tl_graph g, void *stream);
 int tl_graph_destroy(tl_graph g);
 
@@ -134,6 +134,24 @@ int tl_graph_destroy(tl_graph g);
  * relayout (tensor.py:167-184) and view materialisation (contraction.py:
  * 539-542) for the container layer. */
 int tl_copy(const tl_desc *a, const void *a_ptr, const tl_desc *c, void *c_ptr, void *stream);
+
+/* rank_one_compose -- hopm.py:123-139: out (dense first-order, shape of
+ * `shape`) = scale * u_1(i_1) * ... * u_p(i_p), multiplied left to right like
+ * the reference.  u: p device float64 vectors; scale_dev: device double. */
+int tl_rank_one_compose(const tl_desc *shape, const double *const *u, const double *scale_dev, double *out,
+                        void *stream);
+
+/* residual -- hopm.py:142-147: *result_dev = ||A - scale * u_1 o ... o u_p||_F
+ * (elementwise differences exactly as the reference forms them; the sum is
+ * double-double).  ws: tl_reduce_workspace_bytes() zeroed bytes. */
+int tl_residual(const tl_desc *a, const void *a_ptr, const double *const *u, const double *scale_dev,
+                double *result_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* Host only (no device access): the launch plan tl_ttv (op 0) or tl_ttm
+ * (op 1, matrix rows J, matrix descriptor bmat) would use for operand a and
+ * the one-based mode -- the canonical form A[O][K][I], the
+ * kernel regime / GETT digit order -- as a JSON object in buf. */
+int tl_plan_describe(int32_t op, const tl_desc *a, const tl_desc *bmat, int32_t mode, char *buf, size_t len);
 
 #ifdef __cplusplus
 }

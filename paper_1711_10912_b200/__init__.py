@@ -17,7 +17,7 @@ from .contraction import (
     ttm,
     ttv,
 )
-from .hopm import DegenerateInputError, HopmRunner, HopmState, hopm
+from .hopm import DegenerateInputError, HopmRunner, HopmState, hopm, rank_one_compose, residual
 from .layout import (
     MAX_INDEX,
     TensorMeta,
@@ -49,6 +49,8 @@ __all__ = [
     "inverse_memory_index",
     "last_order_layout",
     "memory_index",
+    "rank_one_compose",
+    "residual",
     "tensors_equal",
     "times_matrices",
     "times_vectors",

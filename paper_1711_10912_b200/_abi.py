@@ -37,6 +37,9 @@ EXPORTS = (
     "tl_graph_launch",
     "tl_graph_destroy",
     "tl_copy",
+    "tl_rank_one_compose",
+    "tl_residual",
+    "tl_plan_describe",
 )
 
 
@@ -89,15 +92,20 @@ def load_library(path: str = LIB_PATH):
         L.tl_inner.argtypes = [_dp, _vp, _dp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_frobenius_norm.argtypes = [_dp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_hopm_workspace_bytes.argtypes = [_dp, ctypes.POINTER(ctypes.c_size_t)]
-        L.tl_hopm.argtypes = [_dp, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_double, _vp, _vp, _vp, _vp,
+        vpp = ctypes.POINTER(_vp)
+        L.tl_hopm.argtypes = [_dp, _vp, vpp, vpp, ctypes.c_int32, ctypes.c_double, _vp, _vp, _vp, _vp, _vp,
                               ctypes.c_size_t, _vp]
-        L.tl_hopm_graph_create.argtypes = [_dp, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_double, _vp, _vp,
-                                           _vp, _vp, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)]
+        L.tl_hopm_graph_create.argtypes = [_dp, _vp, vpp, vpp, ctypes.c_int32, ctypes.c_double, _vp, _vp, _vp, _vp,
+                                           _vp, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)]
         L.tl_graph_launch.argtypes = [_vp, _vp]
         L.tl_graph_destroy.argtypes = [_vp]
         L.tl_copy.argtypes = [_dp, _vp, _dp, _vp, _vp]
+        L.tl_rank_one_compose.argtypes = [_dp, vpp, _vp, _vp, _vp]
+        L.tl_residual.argtypes = [_dp, _vp, vpp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+        L.tl_plan_describe.argtypes = [ctypes.c_int32, _dp, _dp, ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
         for name in ("tl_ttv", "tl_ttm", "tl_inner", "tl_frobenius_norm", "tl_hopm_workspace_bytes", "tl_hopm",
-                     "tl_hopm_graph_create", "tl_graph_launch", "tl_graph_destroy", "tl_copy"):
+                     "tl_hopm_graph_create", "tl_graph_launch", "tl_graph_destroy", "tl_copy", "tl_rank_one_compose",
+                     "tl_residual", "tl_plan_describe"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L

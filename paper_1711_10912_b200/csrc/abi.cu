@@ -30,9 +30,16 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
                    bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st);
 int hopm_workspace(const tl_desc &a, size_t *bytes);
 int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, double *const *u, int32_t max_sweeps,
-                 double tol, double *l,
-                 double *hist, int32_t *info, void *ws, size_t ws_bytes, cudaStream_t st);
+                 double tol, double *l, double *hist, int32_t *info, double *resid, void *ws, size_t ws_bytes,
+                 cudaStream_t st);
 int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_ptr, cudaStream_t st);
+int rank_one_enqueue(const tl_desc &shape, const double *const *u, const double *scale_dev, double *out,
+                     cudaStream_t st);
+int residual_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u, const double *scale_dev,
+                     const int32_t *gate, int32_t gate_value, double *result, void *ws, size_t ws_bytes,
+                     cudaStream_t st);
+int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len);
+int ttm_dmma_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out);
 
 static thread_local std::string g_error = "no error";
 
@@ -272,12 +279,24 @@ static int hopm_check(const tl_desc *a, double *const *u_ptrs, int32_t max_sweep
 }
 
 int tl_hopm(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs, double *const *u_ptrs,
-            int32_t max_sweeps, double tol, double *l_dev,
-            double *hist_dev, int32_t *info_dev, void *ws, size_t ws_bytes, void *stream) {
+            int32_t max_sweeps, double tol, double *l_dev, double *hist_dev, int32_t *info_dev, double *resid_dev,
+            void *ws, size_t ws_bytes, void *stream) {
     int rc = hopm_check(a, u_ptrs, max_sweeps);
     if (rc != TL_OK) return rc;
-    return hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, ws, ws_bytes,
-                        (cudaStream_t)stream);
+    return hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, resid_dev, ws,
+                        ws_bytes, (cudaStream_t)stream);
+}
+
+int tl_rank_one_compose(const tl_desc *shape, const double *const *u, const double *scale_dev, double *out,
+                        void *stream) {
+    if (!check_desc(shape, "rank_one shape") || u == nullptr || scale_dev == nullptr) return TL_EINVAL;
+    return rank_one_enqueue(*shape, u, scale_dev, out, (cudaStream_t)stream);
+}
+
+int tl_residual(const tl_desc *a, const void *a_ptr, const double *const *u, const double *scale_dev,
+                double *result_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (!check_desc(a, "residual A") || u == nullptr || scale_dev == nullptr) return TL_EINVAL;
+    return residual_enqueue(*a, a_ptr, u, scale_dev, nullptr, 0, result_dev, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 struct tl_graph_s {
@@ -285,9 +304,8 @@ struct tl_graph_s {
 };
 
 int tl_hopm_graph_create(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs, double *const *u_ptrs,
-                         int32_t max_sweeps, double tol,
-                         double *l_dev, double *hist_dev, int32_t *info_dev, void *ws, size_t ws_bytes, void *stream,
-                         tl_graph *out) {
+                         int32_t max_sweeps, double tol, double *l_dev, double *hist_dev, int32_t *info_dev,
+                         double *resid_dev, void *ws, size_t ws_bytes, void *stream, tl_graph *out) {
     int rc = hopm_check(a, u_ptrs, max_sweeps);
     if (rc != TL_OK) return rc;
     if (out == nullptr) return TL_EINVAL;
@@ -305,7 +323,8 @@ int tl_hopm_graph_create(const tl_desc *a, const void *a_ptr, const double *cons
         if (own) cudaStreamDestroy(cap);
         return cuda_status(e, "hopm begin capture");
     }
-    rc = hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, ws, ws_bytes, cap);
+    rc = hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, resid_dev, ws,
+                      ws_bytes, cap);
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
     if (own) cudaStreamDestroy(cap);
@@ -332,6 +351,30 @@ int tl_graph_destroy(tl_graph g) {
     cudaError_t e = cudaGraphExecDestroy(g->exec);
     delete g;
     return cuda_status(e, "graph destroy");
+}
+
+int tl_plan_describe(int32_t op, const tl_desc *a, const tl_desc *bmat, int32_t mode, char *buf, size_t len) {
+    if (!check_desc(a, "plan A") || buf == nullptr || len == 0) return TL_EINVAL;
+    if (mode < 1 || mode > a->order) {
+        set_error("mode %d out of range 1..%d", mode, a->order);
+        return TL_EINVAL;
+    }
+    if (op == 0) return ttv_describe(*a, mode - 1, buf, len);
+    if (!check_desc(bmat, "plan matrix") || bmat->order != 2 || bmat->extent[1] != a->extent[mode - 1]) {
+        set_error("plan: matrix does not match mode %d", mode);
+        return TL_EINVAL;
+    }
+    std::string s;
+    int rc = ttm_dmma_describe(*a, *bmat, mode - 1, s);
+    if (rc == TL_EUNSUPPORTED) {
+        const int64_t F = volume(*a) / a->extent[mode - 1];
+        s = std::string("{\"path\": \"") + (bmat->extent[0] <= 32 ? "staged" : "simt") + "\", \"F\": " +
+            std::to_string(F) + "}";
+        rc = TL_OK;
+    }
+    if (rc != TL_OK) return rc;
+    snprintf(buf, len, "%s", s.c_str());
+    return TL_OK;
 }
 
 int tl_copy(const tl_desc *a, const void *a_ptr, const tl_desc *c, void *c_ptr, void *stream) {

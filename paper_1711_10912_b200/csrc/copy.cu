@@ -61,8 +61,58 @@ template <class T> __global__ void __launch_bounds__(256) copy_tiled_kernel(cons
     }
 }
 
-template <class T> static cudaError_t launch_copy(const CopyParams &P, bool tiled, int grid, cudaStream_t st) {
-    if (tiled)
+// 64x64 tiles with 16-byte vectors on both sides: the source tile is read
+// along Y (unit stride), written transposed into an XOR-swizzled shared
+// tile, and stored along X (the destination's unit stride).
+constexpr int kCT = 64;
+
+template <class T> __global__ void __launch_bounds__(256) copy_tiled_vec_kernel(const __grid_constant__ CopyParams P) {
+    constexpr int V = 16 / sizeof(T);
+    constexpr int VR = kCT / V;
+    constexpr int NV = kCT * VR / 256;
+    __shared__ __align__(16) T ts[kCT * kCT];  // ts[y][x ^ swz(y)]
+    auto swz = [](int y) { return ((y / V) & 7) * V; };
+    const T *a = (const T *)P.a;
+    T *c = (T *)P.c;
+    const int64_t per_rest = P.tiles_x * P.tiles_y;
+    const int64_t tiles = per_rest * P.n_rest;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t rest = t / per_rest;
+        const int64_t txy = t - rest * per_rest;
+        const int64_t ty = txy / P.tiles_x;
+        const int64_t tx = txy - ty * P.tiles_x;
+        const int64_t x0 = tx * kCT, y0 = ty * kCT;
+        const int64_t ra = P.rest_a.map((uint32_t)rest), rc = P.rest_c.map((uint32_t)rest);
+        T v[NV][V];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int row = e / VR, vc = (e % VR) * V;  // source row x = row, y = vc..
+            *(uint4 *)v[q] = __ldcs((const uint4 *)(a + ra + (x0 + row) * P.a_sX + y0 + vc));
+        }
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int row = e / VR, vc = (e % VR) * V;
+#pragma unroll
+            for (int cc = 0; cc < V; ++cc) ts[(vc + cc) * kCT + (row ^ swz(vc + cc))] = v[q][cc];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int row = e / VR, vc = (e % VR) * V;  // destination row y = row, x = vc..
+            const uint4 w = *(const uint4 *)(ts + row * kCT + (vc ^ swz(row)));
+            __stcs((uint4 *)(c + rc + (y0 + row) * P.c_sY + x0 + vc), w);
+        }
+        __syncthreads();
+    }
+}
+
+template <class T> static cudaError_t launch_copy(const CopyParams &P, int kind, int grid, cudaStream_t st) {
+    if (kind == 2)
+        copy_tiled_vec_kernel<T><<<grid, 256, 0, st>>>(P);
+    else if (kind == 1)
         copy_tiled_kernel<T><<<grid, 256, 0, st>>>(P);
     else
         copy_kernel<T><<<grid, 256, 0, st>>>(P);
@@ -91,10 +141,18 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
         if (a.extent[r] > 1 && (Y < 0 || a.stride[r] < a.stride[Y])) Y = r;
     const int X = dc.empty() ? -1 : dc[0];
     const DeviceInfo &di = device_info();
-    bool tiled = false;
+    int kind = 0;
     int64_t grid;
+    // identical dense layouts: a plain device-to-device copy
+    {
+        std::vector<int> da;
+        bool same = dense_order(a, da) && a.order == c.order;
+        for (int r = 0; same && r < a.order; ++r) same = (a.extent[r] == 1) || (a.stride[r] == c.stride[r]);
+        if (same)
+            return cuda_status(cudaMemcpyAsync(P.c, P.a, (size_t)P.n * s, cudaMemcpyDeviceToDevice, st), "copy");
+    }
     if (X >= 0 && Y >= 0 && X != Y && c.extent[X] >= 8 && c.extent[Y] >= 8) {
-        tiled = true;
+        kind = 1;
         P.nX = c.extent[X];
         P.nY = c.extent[Y];
         P.a_sX = a.stride[X];
@@ -110,9 +168,21 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
         for (auto &d : rc) P.n_rest *= d.first;
         build_map(ra, P.rest_a);
         build_map(rc, P.rest_c);
-        P.tiles_x = (P.nX + 31) / 32;
-        P.tiles_y = (P.nY + 31) / 32;
-        grid = std::min<int64_t>(P.tiles_x * P.tiles_y * P.n_rest, (int64_t)di.num_sms * 16);
+        const int64_t V = 16 / (int64_t)s;
+        bool vec = P.a_sY == 1 && P.nX % kCT == 0 && P.nY % kCT == 0 && P.a_sX % V == 0 && P.c_sY % V == 0 &&
+                   (uintptr_t)P.a % 16 == 0 && (uintptr_t)P.c % 16 == 0;
+        for (auto &d : ra) vec = vec && d.second % V == 0;
+        for (auto &d : rc) vec = vec && d.second % V == 0;
+        if (vec) {
+            kind = 2;
+            P.tiles_x = P.nX / kCT;
+            P.tiles_y = P.nY / kCT;
+            grid = std::min<int64_t>(P.tiles_x * P.tiles_y * P.n_rest, (int64_t)di.num_sms * 4);
+        } else {
+            P.tiles_x = (P.nX + 31) / 32;
+            P.tiles_y = (P.nY + 31) / 32;
+            grid = std::min<int64_t>(P.tiles_x * P.tiles_y * P.n_rest, (int64_t)di.num_sms * 16);
+        }
     } else {
         DigitList la, lc;
         for (int r : dc) {
@@ -131,8 +201,8 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
         grid = std::min<int64_t>((P.n + 255) / 256, (int64_t)di.num_sms * 16);
     }
     cudaError_t e;
-    if (s == 4) e = launch_copy<float>(P, tiled, (int)grid, st);
-    else e = launch_copy<double>(P, tiled, (int)grid, st);  // f64 and i64 move 8-byte words
+    if (s == 4) e = launch_copy<float>(P, kind, (int)grid, st);
+    else e = launch_copy<double>(P, kind, (int)grid, st);  // f64 and i64 move 8-byte words
     return cuda_status(e, "copy launch");
 }
 

@@ -114,8 +114,14 @@ struct HopmLayout {
     size_t ctl_off;
     std::vector<size_t> P_off;  // P_k for k = 2..p at index k
     size_t ping_off, pong_off;
+    size_t red_off;
     size_t total;
 };
+
+size_t reduce_workspace_bytes();
+int residual_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u, const double *scale_dev,
+                     const int32_t *gate, int32_t gate_value, double *result, void *ws, size_t ws_bytes,
+                     cudaStream_t st);
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -151,6 +157,8 @@ static HopmLayout hopm_layout(const tl_desc &a) {
     off += align256((size_t)mx * 8);
     L.pong_off = off;
     off += align256((size_t)mx * 8);
+    L.red_off = off;  // residual reduction scratch (track_residuals)
+    off += align256(reduce_workspace_bytes());
     L.total = off;
     return L;
 }
@@ -161,7 +169,8 @@ int hopm_workspace(const tl_desc &a, size_t *bytes) {
 }
 
 int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, double *const *u, int32_t max_sweeps,
-                 double tol, double *l, double *hist, int32_t *info, void *ws, size_t ws_bytes, cudaStream_t st) {
+                 double tol, double *l, double *hist, int32_t *info, double *resid, void *ws, size_t ws_bytes,
+                 cudaStream_t st) {
     const int p = a.order;
     HopmLayout L = hopm_layout(a);
     if (ws == nullptr || ws_bytes < L.total) {
@@ -172,6 +181,8 @@ int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, d
     HopmCtl *ctl = (HopmCtl *)(base + L.ctl_off);
     cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(HopmCtl), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), st);
+    if (e == cudaSuccess && resid != nullptr)
+        e = cudaMemsetAsync(base + L.red_off, 0, reduce_workspace_bytes(), st);
     for (int r = 0; u0 != nullptr && r < p && e == cudaSuccess; ++r)
         e = cudaMemcpyAsync(u[r], u0[r], (size_t)a.extent[r] * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_status(e, "hopm init");
@@ -247,6 +258,13 @@ int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, d
             hopm_normalize_kernel<<<1, 256, 0, st>>>(wsrc, n, u[r], l, r, p, hist, info, ctl, sweep, tol);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_status(e, "hopm normalize");
+        }
+        if (resid != nullptr) {
+            // residual(a, state) after the sweep (hopm.py:114-115): runs only if
+            // this sweep completed (info[0] == sweep), before the tol check stops
+            int rc = residual_enqueue(a, a_ptr, (const double *const *)u, l + (p - 1), info, sweep,
+                                      resid + (sweep - 1), base + L.red_off, reduce_workspace_bytes(), st);
+            if (rc != TL_OK) return rc;
         }
     }
     return TL_OK;

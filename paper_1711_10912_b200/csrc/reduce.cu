@@ -368,6 +368,170 @@ __global__ void __launch_bounds__(256) dot_tiled_vec_kernel(const __grid_constan
     finish(P, acc);
 }
 
+size_t reduce_workspace_bytes();
+
+// ------------------------------------------------------------ rank one / residual
+// rank_one_compose (hopm.py:123-139): B(i) = scale * u_1(i_1) * ... * u_p(i_p),
+// multiplied left to right exactly as the reference does; residual
+// (hopm.py:142-147): ||A - B||_F without materialising B.  A is walked in its
+// memory order along rows of its fastest dimension; each element's
+// multi-index comes from a digit decode of the row index.
+struct RankOneParams {
+    const void *a;        // residual: A (any dense layout); compose: unused
+    double *out;          // compose: first-order B
+    const double *u[TL_MAX_ORDER];
+    const double *scale;  // device scalar (graph-capturable)
+    const int32_t *gate;  // residual inside HOPM: run only if *gate == gate_value
+    int32_t gate_value;
+    int32_t p;
+    int32_t fast;          // dimension walked along rows
+    int64_t row_len, n_rows;
+    FastDiv rdiv[TL_MAX_ORDER];  // row index -> indices of the other dims (storage order)
+    int32_t rdim[TL_MAX_ORDER];
+    int32_t nrd;
+    int64_t out_stride[TL_MAX_ORDER];  // compose: first-order strides
+    // reduction plumbing (residual)
+    double *result;
+    double *partials;
+    unsigned int *ticket;
+};
+
+__device__ __forceinline__ void rank_one_row(const RankOneParams &P, int64_t row, int32_t *idx) {
+    uint32_t x = (uint32_t)row;
+    for (int d = 0; d < P.nrd; ++d) {
+        uint32_t q, r;
+        if (d == P.nrd - 1) {
+            r = x;
+            q = 0;
+        } else {
+            P.rdiv[d].divmod(x, q, r);
+        }
+        idx[P.rdim[d]] = (int32_t)r;
+        x = q;
+    }
+}
+
+__global__ void __launch_bounds__(256) rank_one_compose_kernel(const __grid_constant__ RankOneParams P) {
+    const double scale = *P.scale;
+    int32_t idx[TL_MAX_ORDER];
+    const int64_t total = P.n_rows * P.row_len;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / P.row_len, c = e - row * P.row_len;
+        rank_one_row(P, row, idx);
+        idx[P.fast] = (int32_t)c;
+        double v = scale;
+        int64_t off = 0;
+        for (int r = 0; r < P.p; ++r) {
+            v = __dmul_rn(v, P.u[r][idx[r]]);
+            off += (int64_t)idx[r] * P.out_stride[r];
+        }
+        P.out[off] = v;
+    }
+}
+
+template <class TA>
+__global__ void __launch_bounds__(256) residual_kernel(const __grid_constant__ RankOneParams P) {
+    if (P.gate != nullptr && *(volatile const int32_t *)P.gate != P.gate_value) return;
+    const double scale = *P.scale;
+    const TA *a = (const TA *)P.a;
+    DD acc{0.0, 0.0};
+    int32_t idx[TL_MAX_ORDER];
+    const int64_t total = P.n_rows * P.row_len;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / P.row_len, c = e - row * P.row_len;
+        rank_one_row(P, row, idx);
+        idx[P.fast] = (int32_t)c;
+        double v = scale;
+        for (int r = 0; r < P.p; ++r) v = __dmul_rn(v, P.u[r][idx[r]]);
+        const double d = __dsub_rn((double)a[e], v);  // A's memory order == e
+        dd_add_prod(acc, d, d);
+    }
+    ReduceParams R{};
+    R.result = P.result;
+    R.partials = P.partials;
+    R.ticket = P.ticket;
+    R.sqrt_result = 1;
+    finish(R, block_reduce(acc));
+}
+
+static bool rank_one_plan(const tl_desc &a, RankOneParams &P) {
+    std::vector<int> dims;
+    if (!dense_order(a, dims)) return false;
+    P.p = a.order;
+    if (dims.empty()) {  // all extents 1
+        P.fast = 0;
+        P.row_len = 1;
+        P.n_rows = 1;
+        P.nrd = 0;
+        return true;
+    }
+    P.fast = dims[0];
+    P.row_len = a.extent[dims[0]];
+    P.n_rows = volume(a) / P.row_len;
+    if (P.n_rows > 0xffffffffll) return false;
+    P.nrd = 0;
+    for (size_t d = 1; d < dims.size(); ++d) {
+        P.rdiv[P.nrd].init((uint32_t)a.extent[dims[d]]);
+        P.rdim[P.nrd] = dims[d];
+        ++P.nrd;
+    }
+    return true;
+}
+
+int rank_one_enqueue(const tl_desc &shape, const double *const *u, const double *scale_dev, double *out,
+                     cudaStream_t st) {
+    RankOneParams P{};
+    tl_desc fo = shape;  // first-order output
+    int64_t run = 1;
+    for (int r = 0; r < fo.order; ++r) {
+        fo.stride[r] = run;
+        P.out_stride[r] = run;
+        run *= fo.extent[r];
+    }
+    if (!rank_one_plan(fo, P)) return TL_EUNSUPPORTED;
+    for (int r = 0; r < fo.order; ++r) P.u[r] = u[r];
+    P.scale = scale_dev;
+    P.out = out;
+    const int64_t total = P.n_rows * P.row_len;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)device_info().num_sms * 8));
+    rank_one_compose_kernel<<<(unsigned)grid, 256, 0, st>>>(P);
+    return cuda_status(cudaGetLastError(), "rank_one_compose launch");
+}
+
+int residual_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u, const double *scale_dev,
+                     const int32_t *gate, int32_t gate_value, double *result, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+    if (ws == nullptr || ws_bytes < reduce_workspace_bytes()) {
+        set_error("residual: workspace of %zu bytes required", reduce_workspace_bytes());
+        return TL_EWORKSPACE;
+    }
+    RankOneParams P{};
+    if (!rank_one_plan(a, P)) {
+        set_error("residual: A must be a dense permutation layout");
+        return TL_EUNSUPPORTED;
+    }
+    for (int r = 0; r < a.order; ++r) P.u[r] = u[r];
+    P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)dtype_size(a.dtype);
+    P.scale = scale_dev;
+    P.gate = gate;
+    P.gate_value = gate_value;
+    P.result = result;
+    P.partials = (double *)ws;
+    P.ticket = (unsigned int *)((unsigned char *)ws + (size_t)kMaxPartials * 2 * sizeof(double));
+    const int64_t total = P.n_rows * P.row_len;
+    const int64_t grid =
+        std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, std::min<int64_t>(device_info().num_sms * 4, kMaxPartials)));
+    if (a.dtype == TL_F32)
+        residual_kernel<float><<<(unsigned)grid, 256, 0, st>>>(P);
+    else if (a.dtype == TL_F64)
+        residual_kernel<double><<<(unsigned)grid, 256, 0, st>>>(P);
+    else {
+        set_error("residual requires floating elements");
+        return TL_EUNSUPPORTED;
+    }
+    return cuda_status(cudaGetLastError(), "residual launch");
+}
+
 // ------------------------------------------------------------ planning
 size_t reduce_workspace_bytes() { return (size_t)kMaxPartials * 2 * sizeof(double) + 256; }
 

@@ -27,6 +27,7 @@
 // parity is checked at 1e-12 of that bound (tests/).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "plan.h"
@@ -299,8 +300,21 @@ struct Digit {
     int64_t ext, as, cs;  // extent, A stride, C stride
 };
 
+static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
+                    cudaStream_t st, std::string *describe);
+
 int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
                      cudaStream_t st) {
+    return gett_run(a, a_ptr, bm, b_ptr, c_ptr, m0, st, nullptr);
+}
+
+// Host-only: the GETT plan (digit order sigma, operand majors, 16-byte pairs).
+int ttm_dmma_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out) {
+    return gett_run(a, (const void *)0x100000, bm, (const void *)0x200000, nullptr, m0, nullptr, &out);
+}
+
+static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
+                    cudaStream_t st, std::string *describe) {
     using namespace gett;
     const int64_t J = bm.extent[0];
     Canon cn;
@@ -391,6 +405,20 @@ int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
         pairs = pairs && (cn.K % 2 == 0) && (P.bs0 % 2 == 0);
     else
         pairs = pairs && (P.bs0 == 1) && (J % 2 == 0) && (P.bs1 % 2 == 0);
+    if (describe != nullptr) {
+        char buf[1024];
+        int n = snprintf(buf, sizeof(buf), "{\"path\": \"gett\", \"O\": %lld, \"K\": %lld, \"I\": %lld, \"J\": %lld, "
+                         "\"jstride\": %lld, \"a_kmajor\": %d, \"b_kmajor\": %d, \"pairs\": %d, \"grid\": %lld, "
+                         "\"sigma\": [",
+                         (long long)cn.O, (long long)cn.K, (long long)cn.I, (long long)J, (long long)cn.jstride,
+                         a_kmajor ? 1 : 0, b_kmajor ? 1 : 0, pairs ? 1 : 0, (long long)grid);
+        for (size_t d = 0; d < sigma.size() && n < (int)sizeof(buf) - 64; ++d)
+            n += snprintf(buf + n, sizeof(buf) - n, "%s[%lld, %lld, %lld]", d ? ", " : "", (long long)sigma[d].ext,
+                          (long long)sigma[d].as, (long long)sigma[d].cs);
+        snprintf(buf + n, sizeof(buf) - n, "]}");
+        *describe = buf;
+        return TL_OK;
+    }
     auto go = [&](auto kern) -> int {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
         if (e != cudaSuccess) return cuda_status(e, "ttm smem attribute");

@@ -635,12 +635,8 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
     }
 }
 
-// Entry used by tl_ttv and by the HOPM orchestration (which passes a stop
-// flag and binary64 outputs for float32 storage).
-int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
-                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
-                const FusedNorm *fn) {
-    Canon cn;
+// Canonical form + kernel choice (host only; no device access).
+static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch &L, Canon &cn) {
     if (!canon_contraction(a, m0, 0, cn)) {
         set_error("ttv: operand A is not a dense permutation layout (materialise views first)");
         return TL_EUNSUPPORTED;
@@ -650,15 +646,9 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         return TL_EUNSUPPORTED;
     }
     const DeviceInfo &di = device_info();
-    TtvLaunch L{};
     TtvParams &P = L.P;
     const size_t s = dtype_size(a.dtype);
     P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)s;
-    P.b = b_ptr;
-    P.c = c_ptr;
-    P.stop = stop;
-    P.b_stride = b_stride;
-    P.b_dtype = b_dtype;
     P.O = cn.O;
     P.K = cn.K;
     P.I = cn.I;
@@ -671,8 +661,8 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     const uintptr_t base = (uintptr_t)P.a;
     bool ok;
     const size_t small_bbytes = ((size_t)P.K * 8 + 15) & ~(size_t)15;
-    const bool small_cols = P.I >= 32 && P.O * P.I <= 8192;
-    const bool small_rows = P.I == 1 && P.O <= 8192;
+    const bool small_cols = P.I >= 32 && P.O * P.I <= 4096;
+    const bool small_rows = P.I == 1 && P.O <= 4096;
     if ((small_cols || small_rows) && P.K <= kSmallSlab * kSmallMaxSlabs &&
         small_bbytes + 32 * (size_t)(P.K | 1) * s <= 200 * 1024) {
         // few outputs: whole 32-output input blocks in flight, one fold warp
@@ -695,6 +685,47 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         set_error("ttv: no launch plan");
         return TL_EUNSUPPORTED;
     }
+    return TL_OK;
+}
+
+static const char *ttv_regime_name(const TtvLaunch &L) {
+    switch (L.regime) {
+        case 0: return "strided";
+        case 1: return L.bulk ? "staged-bulk" : "staged";
+        case 2: return "small-cols";
+        default: return "small-rows";
+    }
+}
+
+// Host-only description of the plan (tl_plan_describe).
+int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
+    TtvLaunch L{};
+    Canon cn;
+    int rc = ttv_make_plan(a, (const void *)0x100000, m0, L, cn);
+    if (rc != TL_OK) return rc;
+    snprintf(buf, len, "{\"O\": %lld, \"K\": %lld, \"I\": %lld, \"ident\": %d, \"inner_digits\": %d, "
+             "\"outer_digits\": %d, \"regime\": \"%s\", \"vec\": %d, \"grid\": %u, \"block\": %u, \"smem\": %zu}",
+             (long long)cn.O, (long long)cn.K, (long long)cn.I, cn.ident ? 1 : 0, (int)cn.inner.size(),
+             (int)cn.outer.size(), ttv_regime_name(L), L.vec, L.grid.x, L.block.x, L.smem);
+    return TL_OK;
+}
+
+// Entry used by tl_ttv and by the HOPM orchestration (which passes a stop
+// flag and binary64 outputs for float32 storage).
+int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
+                int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
+                const FusedNorm *fn) {
+    TtvLaunch L{};
+    Canon cn;
+    int rc = ttv_make_plan(a, a_ptr, m0, L, cn);
+    if (rc != TL_OK) return rc;
+    TtvParams &P = L.P;
+    if (P.O * P.I == 0) return TL_OK;
+    P.b = b_ptr;
+    P.c = c_ptr;
+    P.stop = stop;
+    P.b_stride = b_stride;
+    P.b_dtype = b_dtype;
     if (fn != nullptr && fn->enabled) {
         // the last CTA stages w (= this ttv's output) in its shared memory
         P.fn = *fn;

@@ -1,9 +1,10 @@
 """Higher-order power method on B200 (hopm.py:63-120 of the reference).
 
 The whole Gauss-Seidel loop -- per-mode ttv chains, sequential norms,
-normalisation, lambda history, the tol test and degeneracy -- is one CUDA
-graph built by the C ABI (tl_hopm_graph_create); the host waits once at
-the end.  Results are bit-identical to the reference (csrc/hopm.cu).
+normalisation, lambda history, the tol test, degeneracy and (optionally) the
+per-sweep residual -- is one CUDA graph built by the C ABI
+(tl_hopm_graph_create); the host waits once at the end.  lambda and the
+vectors are bit-identical to the reference (csrc/hopm.cu).
 """
 
 from __future__ import annotations
@@ -16,9 +17,10 @@ from typing import List, Optional, Sequence
 import torch
 
 from . import _abi
+from .layout import TensorMeta
 from .tensor import DenseTensor
 
-__all__ = ["DegenerateInputError", "HopmState", "hopm", "HopmRunner"]
+__all__ = ["DegenerateInputError", "HopmState", "hopm", "HopmRunner", "rank_one_compose", "residual"]
 
 
 class DegenerateInputError(ArithmeticError):
@@ -77,11 +79,16 @@ def _start_vectors(shape, u0) -> List[List[float]]:
     return out
 
 
+def _vec(t: torch.Tensor) -> DenseTensor:
+    return DenseTensor._wrap(TensorMeta((t.numel(),)), t)
+
+
 class HopmRunner:
     """A captured HOPM graph over a fixed tensor: ``run()`` replays the
     whole max_sweeps loop (start vectors are re-copied each replay)."""
 
-    def __init__(self, a: DenseTensor, max_sweeps: int = 50, u0=None, tol: float = 1e-10):
+    def __init__(self, a: DenseTensor, max_sweeps: int = 50, u0=None, tol: float = 1e-10,
+                 track_residuals: bool = False):
         if max_sweeps < 1:
             raise ValueError("max_sweeps must be >= 1")
         if a.dtype not in (torch.float32, torch.float64):
@@ -97,6 +104,7 @@ class HopmRunner:
         self.l = torch.zeros(p, dtype=torch.float64, device=dev)
         self.hist = torch.zeros(self.max_sweeps, dtype=torch.float64, device=dev)
         self.info = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.resid = torch.zeros(self.max_sweeps, dtype=torch.float64, device=dev) if track_residuals else None
         L = _abi.lib()
         desc = a.desc()
         need = ctypes.c_size_t(0)
@@ -109,6 +117,7 @@ class HopmRunner:
         self.stream.wait_stream(torch.cuda.current_stream(dev))
         rc = L.tl_hopm_graph_create(desc, a.ptr(), self._u0p, self._up, self.max_sweeps, self.tol,
                                     self.l.data_ptr(), self.hist.data_ptr(), self.info.data_ptr(),
+                                    self.resid.data_ptr() if self.resid is not None else None,
                                     self.ws.data_ptr(), self.ws.numel(), _abi.stream_handle(self.stream),
                                     ctypes.byref(self._graph))
         _abi.check(rc, "hopm graph")
@@ -118,14 +127,13 @@ class HopmRunner:
         _abi.check(_abi.lib().tl_graph_launch(self._graph, _abi.stream_handle(s)), "hopm launch")
 
     def state(self) -> HopmState:
-        info = self.info.cpu().tolist()
-        sweeps, converged, dsweep, dmode = info
+        sweeps, converged, dsweep, dmode = self.info.cpu().tolist()
         if dsweep:
             raise DegenerateInputError(dsweep, dmode)
-        l = self.l.cpu().tolist()
-        hist = self.hist[:sweeps].cpu().tolist()
-        us = [DenseTensor._wrap(_vec_meta(t.numel()), t.clone()) for t in self.u]
-        return HopmState(u=us, l=l, sweeps=sweeps, converged=bool(converged), lambda_history=hist)
+        resid = self.resid[:sweeps].cpu().tolist() if self.resid is not None else []
+        return HopmState(u=[_vec(t.clone()) for t in self.u], l=self.l.cpu().tolist(), sweeps=sweeps,
+                         converged=bool(converged), lambda_history=self.hist[:sweeps].cpu().tolist(),
+                         residual_history=resid)
 
     def run(self) -> HopmState:
         self.launch()
@@ -143,24 +151,50 @@ class HopmRunner:
             pass
 
 
-def _vec_meta(n):
-    from .layout import TensorMeta
-
-    return TensorMeta((n,))
-
-
 def hopm(a, max_sweeps: int = 50, u0: Optional[Sequence] = None, tol: float = 1e-10,
          track_residuals: bool = False) -> HopmState:
     """Best rank-one approximation by alternating sweeps (hopm.py:63-120).
 
     Raises DegenerateInputError when a mode update has norm zero, ValueError
-    for max_sweeps < 1 or invalid start vectors."""
+    for max_sweeps < 1 or invalid start vectors.  With track_residuals the
+    residual ||a - lambda u_1 o ... o u_p||_F after every sweep is recorded
+    (computed on the device inside the same graph)."""
     if max_sweeps < 1:
         raise ValueError("max_sweeps must be >= 1")
-    if track_residuals:
-        raise NotImplementedError("track_residuals is outside the B200 hot path (hopm.py:142-147)")
-    runner = HopmRunner(a, max_sweeps=max_sweeps, u0=u0, tol=tol)
+    runner = HopmRunner(a, max_sweeps=max_sweeps, u0=u0, tol=tol, track_residuals=track_residuals)
     try:
         return runner.run()
     finally:
         runner.close()
+
+
+def _vector_ptrs(vectors, device):
+    vs = [v.buffer if isinstance(v, DenseTensor) else torch.as_tensor(v) for v in vectors]
+    vs = [v.to(device=device, dtype=torch.float64).contiguous() for v in vs]
+    return vs, (ctypes.c_void_p * len(vs))(*[v.data_ptr() for v in vs])
+
+
+def rank_one_compose(scale: float, vectors: Sequence) -> DenseTensor:
+    """B(i_1, .., i_p) = scale * u_1(i_1) * ... * u_p(i_p), first-order
+    (hopm.py:123-139), multiplied left to right like the reference."""
+    if len(vectors) == 0:
+        raise ValueError("need at least one vector")
+    shape = tuple(int(v.size) if isinstance(v, DenseTensor) else len(v) for v in vectors)
+    out = DenseTensor(shape, fill_value=None)
+    vs, ptrs = _vector_ptrs(vectors, out.device)
+    sc = torch.tensor([float(scale)], dtype=torch.float64, device=out.device)
+    rc = _abi.lib().tl_rank_one_compose(out.desc(), ptrs, sc.data_ptr(), out.ptr(), _abi.stream_handle())
+    _abi.check(rc, "rank_one_compose")
+    return out
+
+
+def residual(a, state: HopmState) -> float:
+    """||a - rank_one_compose(state.scale, state.u)||_F (hopm.py:142-147)."""
+    vs, ptrs = _vector_ptrs(state.u, a.device)
+    sc = torch.tensor([float(state.l[-1])], dtype=torch.float64, device=a.device)
+    res = torch.empty(1, dtype=torch.float64, device=a.device)
+    ws = _abi.reduce_workspace(a.device)
+    rc = _abi.lib().tl_residual(a.desc(), a.ptr(), ptrs, sc.data_ptr(), res.data_ptr(), ws.data_ptr(), ws.numel(),
+                                _abi.stream_handle())
+    _abi.check(rc, "residual")
+    return res.item()

@@ -190,6 +190,20 @@ def make_small():
         l=np.asarray(st.l, dtype=np.float64), lambda_history=np.asarray(st.lambda_history, dtype=np.float64),
         sweeps=st.sweeps, converged=st.converged)
 
+    # hopm with track_residuals, and rank_one_compose (hopm.py:114-115, 123-147)
+    for shape, sweeps in [((4, 3, 5), 6), ((3, 4), 5), ((2, 3, 4, 2), 4)]:
+        p = len(shape)
+        la = W.random_layout(p, rng.randint(0, 10**6))
+        T = draw(nrng, shape, "float64")
+        A = ref.DenseTensor.from_memory(shape, to_ref_values(W.layout_buffer(T, la), "float64"), layout=la)
+        st = ref.hopm(A, max_sweeps=sweeps, tol=0.0, track_residuals=True)
+        B = ref.rank_one_compose(st.scale, st.u)
+        add("hopm_resid", kind="float64", shape=list(shape), layout=list(la), max_sweeps=sweeps, tol=0.0,
+            a=W.layout_buffer(T, la), residual_history=np.asarray(st.residual_history, dtype=np.float64),
+            lambda_history=np.asarray(st.lambda_history, dtype=np.float64),
+            u=np.concatenate([np.asarray(u.data, dtype=np.float64) for u in st.u]),
+            compose=np.asarray(B.data, dtype=np.float64), residual=ref.residual(A, st))
+
     # medium cases exercising each kernel regime (contracted stride 1 / strided;
     # small and wide inner blocks; odd extents)
     medium = [((40, 33, 17), (1, 2, 3), 1), ((40, 33, 17), (1, 2, 3), 2), ((40, 33, 17), (3, 2, 1), 1),

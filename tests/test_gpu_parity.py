@@ -135,6 +135,56 @@ def test_hopm_golden_bit_exact(gpu, small_golden):
     assert n >= 8
 
 
+def test_hopm_residuals_and_rank_one_golden(gpu, small_golden):
+    """track_residuals / residual / rank_one_compose (hopm.py:114-147): lambda
+    and vectors bit-exact, the composed tensor bit-exact (same product order),
+    residuals (a parallel sum) within 1e-12 relative."""
+    m = tl()
+    n = 0
+    for c in small_golden["cases"]:
+        if c["op"] != "hopm_resid":
+            continue
+        A = dev_tensor(c["a"], c["shape"], c["layout"])
+        st = m.hopm(A, max_sweeps=c["max_sweeps"], tol=c["tol"], track_residuals=True)
+        assert np.array_equal(bits(np.asarray(st.lambda_history)), bits(c["lambda_history"]))
+        assert np.array_equal(bits(np.concatenate([u.numpy() for u in st.u])), bits(c["u"]))
+        assert len(st.residual_history) == len(c["residual_history"])
+        for got, want in zip(st.residual_history, c["residual_history"]):
+            assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+        B = m.rank_one_compose(st.scale, st.u)
+        assert B.shape == tuple(c["shape"]) and np.array_equal(bits(B.numpy()), bits(c["compose"]))
+        assert abs(m.residual(A, st) - c["residual"]) <= 1e-12 * max(1.0, c["residual"])
+        n += 1
+    assert n == 3
+
+
+def test_cli_hopm(gpu, tmp_path, capsys):
+    """`python -m paper_1711_10912_b200 hopm` mirrors cli.py:139-164."""
+    import json
+
+    from paper_1711_10912_b200 import cli
+
+    rng = np.random.default_rng(8)
+    us = [rng.standard_normal(n) for n in (3, 4, 2)]
+    us = [u / np.linalg.norm(u) for u in us]
+    T = 2.0 * np.einsum("i,j,k->ijk", *us)
+    path = tmp_path / "t.json"
+    path.write_text(json.dumps({"shape": [3, 4, 2], "layout": [1, 2, 3], "offsets": [0, 0, 0],
+                                "data": T.ravel("F").tolist()}))
+    assert cli.main(["hopm", "--in", str(path), "--json"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["converged"] and abs(out["scale"] - 2.0) < 1e-10 and out["residual"] < 1e-10
+    path.write_text(json.dumps({"shape": [2, 3], "data": [0.0] * 6}))
+    assert cli.main(["hopm", "--in", str(path)]) == 3
+    path.write_text(json.dumps({"shape": [3, 3, 3], "data": rng.uniform(-1, 1, 27).tolist()}))
+    assert cli.main(["hopm", "--in", str(path), "--sweeps", "1"]) == 2
+    assert "sweep 1: lambda" in capsys.readouterr().out
+    path.write_text("{not json")
+    with pytest.raises(SystemExit) as e:
+        cli.main(["hopm", "--in", str(path)])
+    assert e.value.code == 1
+
+
 def test_kats(gpu, small_golden):
     m = tl()
     kat = small_golden["kat"]

@@ -71,7 +71,70 @@ def test_abi_validation_mirrors_reference_errors():
     assert L.tl_ttv(a, None, desc((4,)), None, desc((3, 1), (3, 1)), None, 2, None) == _abi.TL_EINVAL
     # hopm max_sweeps < 1 (hopm.py:79-80)
     ptrs = (ctypes.c_void_p * 2)()
-    assert L.tl_hopm(a, None, None, ptrs, 0, 0.0, None, None, None, None, 0, None) == _abi.TL_EINVAL
+    assert L.tl_hopm(a, None, None, ptrs, 0, 0.0, None, None, None, None, None, 0, None) == _abi.TL_EINVAL
+    # host-only plan query rejects a bad mode
+    buf = ctypes.create_string_buffer(256)
+    assert L.tl_plan_describe(0, a, None, 5, buf, 256) == _abi.TL_EINVAL
+
+
+def plan(op, shape, layout, mode, dtype=_abi.TL_F32, bshape=None):
+    import json
+
+    L = _abi.load_library()
+    L.tl_plan_describe.argtypes = [ctypes.c_int32, ctypes.POINTER(_abi.TlDesc), ctypes.POINTER(_abi.TlDesc),
+                                   ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
+    buf = ctypes.create_string_buffer(2048)
+    b = desc(bshape, dtype=dtype) if bshape else None
+    rc = L.tl_plan_describe(op, desc(shape, compute_strides(shape, layout), dtype), b, mode, buf, 2048)
+    assert rc == 0, L.tl_last_error()
+    return json.loads(buf.value.decode())
+
+
+# SURVEY.md §8a canonical forms (A: contracted stride 1 -> staged; B: strided).
+CFG2_TABLE = {
+    (1, 2, 3, 4): [("staged", 2**21, 1, True), ("strided", 2**14, 128, True), ("strided", 128, 2**14, True),
+                   ("strided", 1, 2**21, True)],
+    (4, 3, 2, 1): [("strided", 1, 2**21, False), ("strided", 128, 2**14, False), ("strided", 2**14, 128, False),
+                   ("staged", 2**21, 1, False)],
+    (3, 1, 2, 4): [("strided", 2**14, 128, False), ("strided", 128, 2**14, False), ("staged", 2**21, 1, True),
+                   ("strided", 1, 2**21, False)],
+}
+
+
+@pytest.mark.parametrize("layout", list(CFG2_TABLE))
+def test_ttv_canonical_forms_match_survey(layout):
+    for mode, (regime, O, I, ident) in enumerate(CFG2_TABLE[layout], start=1):
+        p = plan(0, (128,) * 4, layout, mode)
+        assert (p["regime"], p["O"], p["K"], p["I"], bool(p["ident"])) == (regime, O, 128, I, ident), (layout, mode)
+
+
+def test_ttv_plans_for_other_configs():
+    # config 1: O=64, K=96, I=128 (regime B)
+    p = plan(0, (128, 96, 64), (1, 2, 3), 2, _abi.TL_F64)
+    assert (p["regime"], p["O"], p["K"], p["I"]) == ("strided", 64, 96, 128)
+    # config 5 seed 0 layout: contracted stride 1, K=9, permuted output, TMA bulk tiles
+    shape5 = (3, 33, 5, 17, 9, 2, 640)
+    p = plan(0, shape5, (5, 3, 2, 1, 6, 4, 7), 5, _abi.TL_F64)
+    assert (p["regime"], p["O"], p["K"], p["I"], p["ident"]) == ("staged-bulk", 10771200, 9, 1, 0)
+    # config 5 seed 5 layout: O=1, I=10.7M (regime B)
+    p = plan(0, shape5, (7, 4, 2, 1, 6, 3, 5), 5, _abi.TL_F64)
+    assert (p["regime"], p["O"], p["I"]) == ("strided", 1, 10771200)
+    # HOPM's 400x400 intermediates use the small-problem kernels
+    assert plan(0, (400, 400), (1, 2), 1, _abi.TL_F64)["regime"] == "small-rows"
+    assert plan(0, (400, 400), (1, 2), 2, _abi.TL_F64)["regime"] == "small-cols"
+
+
+def test_ttm_gett_plans():
+    # config 3 on the GETT: operand majors and the free-digit order sigma
+    p = plan(1, (512,) * 3, (1, 2, 3), 1, _abi.TL_F64, (384, 512))
+    assert p["path"] == "gett" and p["a_kmajor"] == 1 and p["jstride"] == 1 and p["pairs"] == 1
+    p = plan(1, (512,) * 3, (1, 2, 3), 2, _abi.TL_F64, (384, 512))
+    assert (p["O"], p["K"], p["I"], p["a_kmajor"]) == (512, 512, 512, 0)
+    # last-order mode 2: A's and C's fastest free dims differ -> 2-D box 8 x 16
+    p = plan(1, (512,) * 3, (3, 2, 1), 2, _abi.TL_F64, (384, 512))
+    assert p["sigma"][0] == [8, 1, 196608] and p["sigma"][1] == [16, 262144, 1]
+    # config 5's ttm (J = 16) is HBM-bound -> staged kernel
+    assert plan(1, (3, 33, 5, 17, 2, 640), (1, 2, 3, 4, 5, 6), 2, _abi.TL_F64, (16, 33))["path"] == "staged"
 
 
 def test_compute_strides_rule_and_erratum():

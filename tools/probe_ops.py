@@ -78,6 +78,15 @@ def main(which):
                 med, _ = timeit(lambda: tl.contraction.inner_product_device(A, Bl))
                 print(f"cfg2 inner fl: {med*1e3:8.1f} us {8*2**28/med/1e6:7.1f} GB/s", flush=True)
                 del B, Bl
+                from paper_1711_10912_b200.tensor import _copy
+                import paper_1711_10912_b200._abi as abi
+
+                for lay in ((4, 3, 2, 1), (3, 1, 2, 4)):
+                    out = torch.empty_like(A.buffer)
+                    cd = abi.make_desc(A.shape, tl.compute_strides(A.shape, lay), abi.TL_F32)
+                    med, _ = timeit(lambda: _copy(A.desc(), A.buffer, cd, out))
+                    print(f"cfg2 relayout first->{lay}: {med*1e3:8.1f} us {8*2**28/med/1e6:7.1f} GB/s", flush=True)
+                    del out
             del A
             torch.cuda.empty_cache()
     if "cfg5" in which:

@@ -178,6 +178,9 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t *bar, uint32_t parity)
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // The barrier's pending count drops when all of this thread's prior cp.async
 // copies have landed (counts as one arrival).

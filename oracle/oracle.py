@@ -247,3 +247,60 @@ def hopm(buf, shape, strides, max_sweeps=50, tol=1e-10, u0=None, nthreads=0):
         "sweeps": sweeps,
         "converged": bool(info[1]),
     }
+
+
+# -- small-case pure-Python restatements (no C counterpart needed at these sizes) -----
+
+
+def _py(buf, kind):
+    arr = np.asarray(buf).reshape(-1)
+    return [int(x) for x in arr] if kind == "int64" else [float(x) for x in arr.astype(np.float64)]
+
+
+def _multi(shape):
+    """Zero-based multi-indices, last dimension fastest."""
+    import itertools
+
+    return itertools.product(*[range(n) for n in shape])
+
+
+def ttt(abuf, ashape, astrides, bbuf, bshape, bstrides, q, phi, psi, kind="float64"):
+    """Tensor-times-tensor (contraction.py:337-418): output = A's free dims
+    in phi order then B's in psi order (first-order buffer); each output is
+    a left fold over the contracted pairs, the LAST pair innermost (the base
+    case of _ttt_rec), as ``acc += a * b`` on Python numbers.  Returns
+    (flat first-order output list, out_shape)."""
+    a, b = _py(abuf, kind), _py(bbuf, kind)
+    phi = [x - 1 for x in phi]
+    psi = [x - 1 for x in psi]
+    r, s = len(phi) - q, len(psi) - q
+    out_shape = tuple(ashape[phi[k]] for k in range(r)) + tuple(bshape[psi[k]] for k in range(s))
+    bounds = [ashape[phi[r + k]] for k in range(q)]
+    shape = out_shape or (1,)
+    fs = first_order_strides(shape)
+    out = [0 if kind == "int64" else 0.0] * int(np.prod(shape))
+    for ic in _multi(shape):
+        pa = sum(ic[k] * astrides[phi[k]] for k in range(r))
+        pb = sum(ic[r + k] * bstrides[psi[k]] for k in range(s))
+        acc = 0 if kind == "int64" else 0.0
+        if q == 0:
+            acc = a[pa] * b[pb]
+        else:
+            for jt in _multi(bounds):  # first contracted pair outermost
+                ia = pa + sum(jt[k] * astrides[phi[r + k]] for k in range(q))
+                ib = pb + sum(jt[k] * bstrides[psi[s + k]] for k in range(q))
+                acc += a[ia] * b[ib]
+        out[sum(i * w for i, w in zip(ic, fs)) if out_shape else 0] = acc
+    return out, out_shape if out_shape else (1,)
+
+
+def transpose(abuf, shape, strides, tau, kind="float64"):
+    """C(i_1..i_p) = A(i_tau1..i_taup), first-order output (contraction.py:75-107)."""
+    a = _py(abuf, kind)
+    out_shape = tuple(shape[t - 1] for t in tau)
+    fs = first_order_strides(out_shape)
+    out = [None] * int(np.prod(out_shape))
+    for ic in _multi(out_shape):
+        pa = sum(ic[r] * strides[t - 1] for r, t in enumerate(tau))
+        out[sum(i * w for i, w in zip(ic, fs))] = a[pa]
+    return out, out_shape

@@ -9,12 +9,18 @@ buffers and streams only.  There is no CPU fallback.
 """
 
 from .contraction import (
+    ContractionSpec,
     frobenius_norm,
     inner_product_flat,
     inner_product_tensors,
+    outer_product,
+    reduce_ttm_to_ttt,
+    reduce_ttv_to_ttt,
     times_matrices,
     times_vectors,
+    transpose,
     ttm,
+    ttt,
     ttv,
 )
 from .hopm import DegenerateInputError, HopmRunner, HopmState, hopm, rank_one_compose, residual
@@ -34,6 +40,12 @@ from .tensor import DenseTensor, tensors_equal
 __version__ = "0.1.0"
 
 __all__ = [
+    "ContractionSpec",
+    "outer_product",
+    "reduce_ttm_to_ttt",
+    "reduce_ttv_to_ttt",
+    "transpose",
+    "ttt",
     "DegenerateInputError",
     "DenseTensor",
     "HopmRunner",

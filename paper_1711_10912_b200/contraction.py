@@ -11,8 +11,9 @@ Every numeric step runs in hand-written sm_100a kernels behind the C ABI
 
 from __future__ import annotations
 
-import ctypes
 import math
+from dataclasses import dataclass
+from typing import Sequence, Tuple
 
 import torch
 
@@ -21,12 +22,18 @@ from .layout import TensorMeta
 from .tensor import DenseTensor, _copy
 
 __all__ = [
+    "ContractionSpec",
     "frobenius_norm",
     "inner_product_flat",
     "inner_product_tensors",
+    "outer_product",
+    "reduce_ttm_to_ttt",
+    "reduce_ttv_to_ttt",
     "times_matrices",
     "times_vectors",
+    "transpose",
     "ttm",
+    "ttt",
     "ttv",
 ]
 
@@ -203,6 +210,141 @@ def times_matrices(a, matrices, modes) -> DenseTensor:
     for m, mat in sorted(zip(modes, matrices), reverse=True, key=lambda x: x[0]):
         result = ttm(result, mat, m)
     return result
+
+
+# -- general tensor-times-tensor ------------------------------
+
+
+@dataclass(frozen=True)
+class ContractionSpec:
+    """q contracted pairs; one-based permutations phi (A) and psi (B), free
+    dimensions first, contracted pairs last (contraction.py:304-334)."""
+
+    q: int
+    phi: Tuple[int, ...]
+    psi: Tuple[int, ...]
+
+    def __post_init__(self):
+        object.__setattr__(self, "phi", tuple(int(x) for x in self.phi))
+        object.__setattr__(self, "psi", tuple(int(x) for x in self.psi))
+        if self.q < 0:
+            raise ValueError("q must be nonnegative")
+        for name, perm in (("phi", self.phi), ("psi", self.psi)):
+            if sorted(perm) != list(range(1, len(perm) + 1)):
+                raise ValueError(f"{name} {perm} is not a permutation")
+        if self.q > len(self.phi) or self.q > len(self.psi):
+            raise ValueError("q exceeds an operand's order")
+        if not self.phi or not self.psi:
+            raise ValueError("operands must have at least one dimension")
+
+    @property
+    def r(self) -> int:
+        return len(self.phi) - self.q
+
+    @property
+    def s(self) -> int:
+        return len(self.psi) - self.q
+
+
+def _relayouted(T: DenseTensor, layout) -> DenseTensor:
+    """A copy of T stored under ``layout`` (device tl_copy)."""
+    if tuple(layout) == T.layout:
+        return T
+    out = DenseTensor(T.shape, layout=tuple(layout), dtype=T.dtype, device=T.device, fill_value=None)
+    _copy(T.desc(), T.buffer, out.desc(), out.buffer)
+    return out
+
+
+def ttt(a, b, spec: ContractionSpec) -> DenseTensor:
+    """General tensor-tensor product (contraction.py:337-369).
+
+    C = A's free dims (phi order) then B's free dims (psi order), summing the
+    q contracted pairs.  On the device this is two relayouts and one ttm:
+    A is stored as a first-order (F_A x K) matrix and B as a (K x F_B)
+    tensor with the contracted index linearised last-pair-fastest -- the
+    reference's nesting order (the innermost loop of _ttt_rec is the last
+    pair) -- and C = ttm(B', A', 1) is already C's first-order buffer."""
+    A, B = _operand(a), _operand(b)
+    q, r, s = spec.q, spec.r, spec.s
+    if len(spec.phi) != A.order:
+        raise ValueError(f"phi length {len(spec.phi)} does not match order {A.order}")
+    if len(spec.psi) != B.order:
+        raise ValueError(f"psi length {len(spec.psi)} does not match order {B.order}")
+    phi = [x - 1 for x in spec.phi]
+    psi = [x - 1 for x in spec.psi]
+    for k in range(q):
+        na, nb = A.shape[phi[r + k]], B.shape[psi[s + k]]
+        if na != nb:
+            raise ValueError(f"contracted pair {k + 1} has mismatched extents {na} vs {nb}")
+    if _is_float(A.dtype) != _is_float(B.dtype):
+        raise NotImplementedError("ttt: mixed integer and floating operands")
+    if B.dtype != A.dtype:
+        B = B.to(A.dtype)
+    out_shape = tuple(A.shape[phi[k]] for k in range(r)) + tuple(B.shape[psi[k]] for k in range(s))
+    L = _abi.lib()
+    code = _abi.DTYPE_CODE[A.dtype]
+
+    def view(T, dims):  # descriptor of T with its dimensions visited in ``dims`` order
+        return _abi.make_desc(tuple(T.shape[d] for d in dims), tuple(T.strides[d] for d in dims), code)
+
+    if r == 0 and s == 0:
+        # full contraction: the inner product over the paired dimensions
+        res = _reduce_result_buffer(A.dtype, A.device)
+        ws = _abi.reduce_workspace(A.device)
+        _abi.check(L.tl_inner(view(A, phi), A.ptr(), view(B, psi), B.ptr(), res.data_ptr(), ws.data_ptr(),
+                              ws.numel(), _abi.stream_handle()), "ttt")
+        return DenseTensor._wrap(TensorMeta((1,)), res.to(A.dtype))
+    if q == 1 and (s == 0 or r == 0):
+        # one operand is a vector: ttv over a permuted view, the reference's
+        # fold bit for bit (x*y commutes)
+        T, perm, v = (A, phi, B) if s == 0 else (B, psi, A)
+        out = DenseTensor(out_shape, dtype=A.dtype, device=A.device, fill_value=None)
+        _abi.check(L.tl_ttv(view(T, perm), T.ptr(), v.desc(), v.ptr(), out.desc(), out.ptr(), len(perm),
+                            _abi.stream_handle()), "ttt")
+        return out
+    FA = math.prod(A.shape[phi[k]] for k in range(r))
+    FB = math.prod(B.shape[psi[k]] for k in range(s))
+    Kq = math.prod(A.shape[phi[r + k]] for k in range(q))
+    a_layout = tuple(phi[k] + 1 for k in range(r)) + tuple(phi[r + k] + 1 for k in reversed(range(q)))
+    b_layout = tuple(psi[s + k] + 1 for k in reversed(range(q))) + tuple(psi[k] + 1 for k in range(s))
+    Am = DenseTensor._wrap(TensorMeta((FA, Kq)), _relayouted(A, a_layout).buffer)
+    Bt = DenseTensor._wrap(TensorMeta((Kq, FB)), _relayouted(B, b_layout).buffer)
+    C = ttm(Bt, Am, 1)  # (FA, FB) first-order == C's first-order buffer
+    return DenseTensor._wrap(TensorMeta(out_shape if out_shape else (1,)), C.buffer)
+
+
+def reduce_ttv_to_ttt(p: int, m: int) -> ContractionSpec:
+    """Spec whose ttt equals ttv(a, b, m) for order-p a (contraction.py:421-426)."""
+    if not 1 <= m <= p:
+        raise ValueError(f"mode {m} out of range 1..{p}")
+    return ContractionSpec(1, tuple(k for k in range(1, p + 1) if k != m) + (m,), (1,))
+
+
+def reduce_ttm_to_ttt(p: int, m: int) -> ContractionSpec:
+    """ttm as ttt with the new dimension last (contraction.py:429-440)."""
+    if not 1 <= m <= p:
+        raise ValueError(f"mode {m} out of range 1..{p}")
+    return ContractionSpec(1, tuple(k for k in range(1, p + 1) if k != m) + (m,), (1, 2))
+
+
+def outer_product(a, b) -> DenseTensor:
+    """All-pairs product: ttt with q = 0 (contraction.py:446-454)."""
+    A, B = _operand(a), _operand(b)
+    return ttt(A, B, ContractionSpec(0, tuple(range(1, A.order + 1)), tuple(range(1, B.order + 1))))
+
+
+def transpose(a, tau: Sequence[int]) -> DenseTensor:
+    """Permuted copy C(i_1..i_p) = A(i_tau1..i_taup), first-order output
+    (contraction.py:75-107): one device copy with permuted source strides."""
+    A = _operand(a)
+    p = A.order
+    tau = tuple(int(t) for t in tau)
+    if sorted(tau) != list(range(1, p + 1)):
+        raise ValueError(f"tau {tau} is not a permutation of 1..{p}")
+    out = DenseTensor(tuple(A.shape[t - 1] for t in tau), dtype=A.dtype, device=A.device, fill_value=None)
+    src = _abi.make_desc(out.shape, tuple(A.strides[t - 1] for t in tau), _abi.DTYPE_CODE[A.dtype])
+    _copy(src, A.buffer, out.desc(), out.buffer)
+    return out
 
 
 def _first_order_copy(A: DenseTensor) -> DenseTensor:

@@ -231,6 +231,45 @@ def make_small():
             a=W.layout_buffer(T, layout), bmat=W.layout_buffer(M, blayout), bshape=[J, shape[mode - 1]],
             out=np.asarray(C.data, dtype=np.float64), out_shape=list(C.shape))
 
+    # ttt (contraction.py:337-418): random q, permutations, layouts; transpose; outer product
+    for t in range(45):
+        kind = "int64" if t % 3 == 2 else ("float32" if t % 3 == 1 else "float64")
+        pa, pb = rng.randint(1, 4), rng.randint(1, 4)
+        q = rng.randint(0, min(pa, pb))
+        phi = tuple(rng.sample(range(1, pa + 1), pa))
+        psi = tuple(rng.sample(range(1, pb + 1), pb))
+        sa = [rng.randint(1, 5) for _ in range(pa)]
+        sb = [rng.randint(1, 5) for _ in range(pb)]
+        for k in range(q):
+            sb[psi[pb - q + k] - 1] = sa[phi[pa - q + k] - 1]
+        la = W.random_layout(pa, rng.randint(0, 10**6))
+        lb = W.random_layout(pb, rng.randint(0, 10**6))
+        Ta, Tb = draw(nrng, tuple(sa), kind), draw(nrng, tuple(sb), kind)
+        A = ref.DenseTensor.from_memory(tuple(sa), to_ref_values(W.layout_buffer(Ta, la), kind), layout=la)
+        B = ref.DenseTensor.from_memory(tuple(sb), to_ref_values(W.layout_buffer(Tb, lb), kind), layout=lb)
+        C = ref.ttt(A, B, ref.ContractionSpec(q, phi, psi))
+        add("ttt", kind=kind, shape=sa, layout=list(la), bshape=sb, blayout=list(lb), q=q, phi=list(phi),
+            psi=list(psi), a=W.layout_buffer(Ta, la), b=W.layout_buffer(Tb, lb),
+            out=np.asarray(C.data, dtype=np.int64 if kind == "int64" else np.float64), out_shape=list(C.shape))
+    for t in range(12):
+        kind = "int64" if t % 2 else "float64"
+        p = rng.randint(1, 5)
+        shape = tuple(rng.randint(1, 5) for _ in range(p))
+        la = W.random_layout(p, rng.randint(0, 10**6))
+        tau = tuple(rng.sample(range(1, p + 1), p))
+        T = draw(nrng, shape, kind)
+        A = ref.DenseTensor.from_memory(shape, to_ref_values(W.layout_buffer(T, la), kind), layout=la)
+        C = ref.transpose(A, tau)
+        add("transpose", kind=kind, shape=list(shape), layout=list(la), tau=list(tau), a=W.layout_buffer(T, la),
+            out=np.asarray(C.data, dtype=np.int64 if kind == "int64" else np.float64), out_shape=list(C.shape))
+    for sa, sb in [((3,), (4,)), ((2, 3), (4,)), ((2,), (3, 2)), ((1, 3), (2, 1, 2))]:
+        Ta, Tb = draw(nrng, sa, "float64"), draw(nrng, sb, "float64")
+        A = ref.DenseTensor.from_memory(sa, Ta.reshape(-1, order="F").tolist())
+        B = ref.DenseTensor.from_memory(sb, Tb.reshape(-1, order="F").tolist())
+        C = ref.outer_product(A, B)
+        add("outer", kind="float64", shape=list(sa), bshape=list(sb), a=Ta.reshape(-1, order="F"),
+            b=Tb.reshape(-1, order="F"), out=np.asarray(C.data, dtype=np.float64), out_shape=list(C.shape))
+
     # known answers restated from the reference's own tests
     I2 = ref.DenseTensor((2, 2))
     I2[0, 0] = 1

@@ -149,3 +149,26 @@ def test_oracle_cfg4(configs_golden):
     assert r["l"] == g["l"]
     for u, want in zip(r["u"], g["u"]):
         assert u.tolist() == want
+
+
+def test_oracle_ttt_transpose_small(small_golden):
+    """The pure-Python ttt / transpose restatements reproduce the
+    reference's outputs bit for bit (contraction.py:75-107, 337-454)."""
+    n = 0
+    for c in small_golden["cases"]:
+        if c["op"] == "ttt":
+            out, shape = O.ttt(c["a"], c["shape"], strides_of(c), c["b"], c["bshape"],
+                               W.compute_strides(c["bshape"], c["blayout"]), c["q"], c["phi"], c["psi"], c["kind"])
+        elif c["op"] == "outer":
+            sa, sb = c["shape"], c["bshape"]
+            out, shape = O.ttt(c["a"], sa, O.first_order_strides(sa), c["b"], sb, O.first_order_strides(sb), 0,
+                               range(1, len(sa) + 1), range(1, len(sb) + 1))
+        elif c["op"] == "transpose":
+            out, shape = O.transpose(c["a"], c["shape"], strides_of(c), c["tau"], c["kind"])
+        else:
+            continue
+        want = c["out"]
+        assert list(shape) == c["out_shape"]
+        assert np.asarray(out, dtype=want.dtype).tobytes() == want.tobytes(), c
+        n += 1
+    assert n >= 60

@@ -1,10 +1,10 @@
 #!/bin/bash
 # One GPU session producing the round's evidence under gpurun_out/:
 #   bench line, ncu launch list of the bench command, ncu --set full of the
-#   ttv kernels (regime S + regime B) and the FP64 GETT, clock samples.
+#   ttv kernels (cfg2), the FP64 GETT (cfg3), the reductions, HOPM and cfg5.
 set -u
 mkdir -p gpurun_out
-timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1
 tail -1 gpurun_out/bench_full.log > gpurun_out/bench_line.json
 CMD="python bench.py --steps 2 --warmup 3 --no-components --no-cpu --no-e2e"
 timeout 300 $CMD > gpurun_out/bench_small.log 2>&1 && \
@@ -12,4 +12,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --c
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/launches_ncu.log 2>&1
 tools/ncu_box.sh prof_ttv "ttv_" cfg2
 tools/ncu_box.sh prof_ttm "ttm_dmma" cfg3
+tools/ncu_box.sh prof_red "dot_" cfg2
+tools/ncu_box.sh prof_hopm "ttv_" cfg4
+tools/ncu_box.sh prof_cfg5 "ttv_|ttm_|dot_" cfg5
+rm -f gpurun_out/*.ncu-rep
 du -sh gpurun_out

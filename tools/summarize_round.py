@@ -141,7 +141,9 @@ def main(tag):
     md = [f"# ncu --set full summary ({tag})", ""]
     summary = {"tag": tag}
     ttv_dram = []
-    for name in ("prof_ttv", "prof_ttm"):
+    names = sorted(f[:-len("_details.csv")] for f in os.listdir(OUT) if f.startswith("prof_") and
+                   f.endswith("_details.csv"))
+    for name in names:
         det = details(name)
         rw = raw(name)
         st = stall_summary(name)

@@ -42,7 +42,9 @@ constexpr int LDW = BN + 4;  // pitch of [k][n] / [k][m] tiles (doubles)
 constexpr int LDK = BK + 4;  // pitch of [n][k] / [m][k] tiles (doubles)
 constexpr int A_TILE = BK * LDW > BN * LDK ? BK * LDW : BN * LDK;  // doubles
 constexpr int B_TILE = BK * LDW > BM * LDK ? BK * LDW : BM * LDK;
-constexpr size_t SMEM = (size_t)NST * (A_TILE + B_TILE) * 8 + (size_t)BN * 16;
+constexpr int CP = BN + 4;   // staged-epilogue row pitch (doubles; = 4 mod 16)
+constexpr size_t SMEM = (size_t)NST * (A_TILE + B_TILE) * 8 + (size_t)BN * 28;
+static_assert(BM * CP <= NST * (A_TILE + B_TILE), "staged C tile must fit the operand stages");
 }  // namespace gett
 
 // warp layout: WM x WN warps, each TM m16 tiles x TN n8 tiles
@@ -63,6 +65,7 @@ struct TtmParams {
     int64_t bs0, bs1;
     int32_t mtiles;
     int32_t nd;  // sigma digits (fastest first)
+    int32_t box_a, box_c, box_s;  // 2-D box: store order swaps its two digits (box_s = 0: none)
     FastDiv dig[TL_MAX_DIGITS + 1];
     int64_t dig_a[TL_MAX_DIGITS + 1];
     int64_t dig_c[TL_MAX_DIGITS + 1];
@@ -93,6 +96,8 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
     double *Bs = As + NST * A_TILE;                  // NST x B_TILE
     int64_t *aoff = (int64_t *)(Bs + NST * B_TILE);  // BN
     int64_t *coff = aoff + BN;                       // BN  (-1: masked column)
+    int64_t *coffp = coff + BN;                      // BN  C offset of store position l
+    int32_t *lpos = (int32_t *)(coffp + BN);         // BN  store position of column n
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -103,9 +108,9 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
     const int64_t m0 = (int64_t)mt * BM;
 
     // column tables for this N tile (sigma-ordered free positions)
-    if (tid < BN) {
-        const int64_t q = nt * BN + tid;
-        int64_t ao = 0, co = -1;
+    auto column_offsets = [&](int64_t q, int64_t &ao, int64_t &co) {
+        ao = 0;
+        co = -1;
         if (q < P.F) {
             uint32_t x = (uint32_t)q;
             co = 0;
@@ -122,8 +127,23 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
                 x = qq;
             }
         }
+    };
+    if (tid < BN) {
+        int64_t ao, co;
+        column_offsets(nt * BN + tid, ao, co);
         aoff[tid] = ao;
         coff[tid] = co;
+        // store order of the staged epilogue: position l of the tile in C
+        // order visits column n = perm(l) (swap the two box digits)
+        int n = tid;
+        if (P.box_s) {
+            const int r = tid % P.box_s;
+            n = tid - r + (r % P.box_c) * P.box_a + r / P.box_c;
+        }
+        int64_t a2, c2;
+        column_offsets(nt * BN + n, a2, c2);
+        coffp[tid] = c2;
+        lpos[n] = tid;
     }
     __syncthreads();
 
@@ -275,21 +295,60 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
     cp_async_wait<0>();
 
     // epilogue: fragments -> first-order C
+    if (P.jstride == 1) {
+        // C contiguous along j: fragment rows already form 64-byte runs
 #pragma unroll
-    for (int i = 0; i < TM; ++i) {
+        for (int i = 0; i < TM; ++i) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = m0 + wm * (16 * TM) + i * 16 + g + 8 * h;
+                if (j >= P.J) continue;
+#pragma unroll
+                for (int jj = 0; jj < TN; ++jj) {
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        const int n = wn * (8 * TN) + jj * 8 + 2 * t + v;
+                        const int64_t co = coff[n];
+                        if (co >= 0) P.c[co + j] = acc[i][jj][2 * h + v];
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // Otherwise stage the tile in shared memory in C order (row m, store
+    // position l, skewed one double per 32 positions: 2 wavefronts per
+    // access both ways) and write whole 256-byte warp runs of C.
+    __syncthreads();  // every warp is done with the operand stages
+    double *cs = As;
+    int ln[TN][2];
+#pragma unroll
+    for (int jj = 0; jj < TN; ++jj)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const int l = lpos[wn * (8 * TN) + jj * 8 + 2 * t + v];
+            ln[jj][v] = l + (l >> 5);
+        }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int64_t j = m0 + wm * (16 * TM) + i * 16 + g + 8 * h;
-            if (j >= P.J) continue;
-            const int64_t jo = j * P.jstride;
+            const int m = wm * (16 * TM) + i * 16 + g + 8 * h;
 #pragma unroll
-            for (int jj = 0; jj < TN; ++jj) {
+            for (int jj = 0; jj < TN; ++jj)
 #pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    const int n = wn * (8 * TN) + jj * 8 + 2 * t + v;
-                    const int64_t co = coff[n];
-                    if (co >= 0) P.c[co + jo] = acc[i][jj][2 * h + v];
-                }
+                for (int v = 0; v < 2; ++v) cs[m * CP + ln[jj][v]] = acc[i][jj][2 * h + v];
+        }
+    __syncthreads();
+    {
+        const int l = tid & (BN - 1);
+        const int64_t co = coffp[l];
+        if (co >= 0) {
+            const double *src = cs + l + (l >> 5);
+#pragma unroll 4
+            for (int m = tid / BN; m < BM; m += THREADS / BN) {
+                const int64_t j = m0 + m;
+                if (j < P.J) P.c[co + j * P.jstride] = src[m * CP];
             }
         }
     }
@@ -342,6 +401,7 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     }
     const bool a_kmajor = (cn.I == 1);
     std::vector<Digit> sigma;
+    bool box = false;
     if (cn.jstride == 1 || dg.empty()) {
         sigma = dg;  // output contiguous along j: keep A's order
     } else if (a_kmajor) {
@@ -358,6 +418,7 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
             // 2-D box: 8 along A's fastest digit (64-byte load runs) x 16
             // along C's fastest digit (whole sectors of C per CTA)
             const Digit dc = dg[ic], da = dg[0];
+            box = true;
             const int64_t alo = (da.ext % 8 == 0 && da.ext > 8) ? 8 : da.ext;
             const int64_t clo = (dc.ext % 16 == 0 && dc.ext > 16) ? 16 : dc.ext;
             sigma.push_back({alo, da.as, da.cs});
@@ -369,6 +430,13 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         }
     }
     if (sigma.size() > TL_MAX_DIGITS + 1) return TL_EUNSUPPORTED;
+    int32_t box_a = 0, box_c = 0, box_s = 0;
+    if (box) {
+        box_a = (int32_t)sigma[0].ext;
+        box_c = (int32_t)sigma[1].ext;
+        box_s = box_a * box_c;
+        if (BN % box_s != 0) box_a = box_c = box_s = 0;
+    }
 
     TtmParams P{};
     P.a = (const double *)a_ptr + a.offset;
@@ -384,6 +452,9 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     P.mtiles = (int32_t)((J + BM - 1) / BM);
     if (sigma.empty()) sigma.push_back({1, 0, 0});
     P.nd = (int32_t)sigma.size();
+    P.box_a = box_a;
+    P.box_c = box_c;
+    P.box_s = box_s;
     for (size_t d = 0; d < sigma.size(); ++d) {
         P.dig[d].init((uint32_t)sigma[d].ext);
         P.dig_a[d] = sigma[d].as;
@@ -408,10 +479,10 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     if (describe != nullptr) {
         char buf[1024];
         int n = snprintf(buf, sizeof(buf), "{\"path\": \"gett\", \"O\": %lld, \"K\": %lld, \"I\": %lld, \"J\": %lld, "
-                         "\"jstride\": %lld, \"a_kmajor\": %d, \"b_kmajor\": %d, \"pairs\": %d, \"grid\": %lld, "
+                         "\"jstride\": %lld, \"a_kmajor\": %d, \"b_kmajor\": %d, \"pairs\": %d, \"grid\": %lld, \"box\": %d, "
                          "\"sigma\": [",
                          (long long)cn.O, (long long)cn.K, (long long)cn.I, (long long)J, (long long)cn.jstride,
-                         a_kmajor ? 1 : 0, b_kmajor ? 1 : 0, pairs ? 1 : 0, (long long)grid);
+                         a_kmajor ? 1 : 0, b_kmajor ? 1 : 0, pairs ? 1 : 0, (long long)grid, (int)box_s);
         for (size_t d = 0; d < sigma.size() && n < (int)sizeof(buf) - 64; ++d)
             n += snprintf(buf + n, sizeof(buf) - n, "%s[%lld, %lld, %lld]", d ? ", " : "", (long long)sigma[d].ext,
                           (long long)sigma[d].as, (long long)sigma[d].cs);

@@ -209,14 +209,22 @@ int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void 
         return TL_EUNSUPPORTED;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    // GEMM-shaped float64 -> DMMA GETT; few rows J -> HBM-bound staged fold;
-    // anything else -> one-thread-per-output fold
+    // few rows J (<= 32): the staged tile kernels (HBM-bound; DMMA for
+    // float64); GEMM-shaped float64 -> DMMA GETT; anything else -> one
+    // thread per output
+    const bool few_rows = bmat->extent[0] <= 32;
+    if (few_rows || a->dtype != TL_F64) {
+        int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+        if (rc != TL_EUNSUPPORTED) return rc;
+    }
     if (a->dtype == TL_F64) {
         int rc = ttm_dmma_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
         if (rc != TL_EUNSUPPORTED) return rc;
+        if (!few_rows) {
+            rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+            if (rc != TL_EUNSUPPORTED) return rc;
+        }
     }
-    int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
-    if (rc != TL_EUNSUPPORTED) return rc;
     return ttm_simt_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
 }
 
@@ -365,7 +373,7 @@ int tl_plan_describe(int32_t op, const tl_desc *a, const tl_desc *bmat, int32_t 
         return TL_EINVAL;
     }
     std::string s;
-    int rc = ttm_dmma_describe(*a, *bmat, mode - 1, s);
+    int rc = bmat->extent[0] <= 32 ? TL_EUNSUPPORTED : ttm_dmma_describe(*a, *bmat, mode - 1, s);
     if (rc == TL_EUNSUPPORTED) {
         const int64_t F = volume(*a) / a->extent[mode - 1];
         s = std::string("{\"path\": \"") + (bmat->extent[0] <= 32 ? "staged" : "simt") + "\", \"F\": " +

@@ -382,8 +382,9 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         return TL_EUNSUPPORTED;
     }
     const int64_t F = cn.O * cn.I;
-    // GEMM-shaped only: small J or K is HBM-bound and goes to the staged kernel
-    if (J < 32 || cn.K < 16 || F < 64 || F > 0xffffffffll) return TL_EUNSUPPORTED;
+    // GEMM-shaped only: few rows J (the caller tries the staged kernel
+    // first for J <= 32) or tiny K / F
+    if (J < 8 || cn.K < 16 || F < 64 || F > 0xffffffffll) return TL_EUNSUPPORTED;
 
     // free digits in A order with A strides
     std::vector<Digit> dg;

@@ -15,6 +15,7 @@
 // ttm_simt: one thread per output, the reference's fold (fallback).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "plan.h"
 #include "tl_common.cuh"
@@ -291,6 +292,151 @@ __global__ void __launch_bounds__(256) ttm_staged_kernel(const __grid_constant__
     cp_async_wait<0>();
 }
 
+// float64, few rows J, output in A's order (ident): the staged DMMA tile
+// with a TMA bulk epilogue.  A tile of R slabs A[o][K][I] arrives by bulk
+// copy; its outputs C[o][J][I] are one contiguous range of first-order C,
+// so the fragments are parked in a double-buffered shared tile and leave in
+// ONE bulk store (instead of 8-byte scattered stores: 32 sectors per warp
+// instruction, the LSU limit of the staged kernel).  Every warp owns a fixed
+// set of 8*NT tile positions, so fragment bases and output offsets are
+// computed once per kernel, not per tile.
+template <int MT, int NT, int NST>
+__global__ void __launch_bounds__(256) ttm_bulk_kernel(const __grid_constant__ TtmSimtParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[NST];
+    const int64_t K = P.K, I = P.I, J = P.J;
+    const int64_t KI = K * I;
+    const int64_t jpad = ttm_jpad(J);
+    const int ldb = (int)ttm_ldb(K);
+    double *bsm = (double *)smem_raw;
+    const size_t bbytes = StagedLayout<double, true>(J, K).bbytes;
+    unsigned char *stages = smem_raw + bbytes;
+    const size_t stage_bytes = ((size_t)P.R * KI * 8 + 15) & ~(size_t)15;
+    const size_t otile = ((size_t)P.R * J * I * 8 + 15) & ~(size_t)15;
+    double *outs = (double *)(stages + NST * stage_bytes);
+
+    for (int64_t e = threadIdx.x; e < jpad * ldb; e += blockDim.x) {
+        const int64_t j = e / ldb, k = e - j * ldb;
+        bsm[e] = (j < J && k < K) ? ((const double *)P.bm)[j * P.bs0 + k * P.bs1] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(&full_bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    auto issue = [&](int64_t q) {
+        const int s = (int)(q % NST);
+        const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
+        const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
+        const uint32_t bytes = (uint32_t)(rows * KI * 8);
+        const uint32_t b16 = bytes & ~15u;
+        unsigned char *dst = stages + s * stage_bytes;
+        const unsigned char *src = (const unsigned char *)((const double *)P.a + o0 * KI);
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], b16);
+            if (b16) bulk_g2s(dst, src, b16, &full_bar[s]);
+        }
+        if (bytes != b16 && threadIdx.x == 0) cp_async<8>(dst + b16, src + b16);
+    };
+#pragma unroll
+    for (int q = 0; q < NST - 1; ++q) {
+        if (q < my_tiles) issue(q);
+        cp_async_commit();
+    }
+
+    // fixed per-lane geometry
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t slots = (uint32_t)(P.R * I);
+    const uint32_t p0 = (uint32_t)warp * (8 * NT);
+    int base[NT];     // B-fragment column (position p0 + 8 nt + g) in the stage
+    bool okp[NT];
+    int orow[NT][2];  // output row r of positions p0 + 8 nt + 2t + v (-1: none)
+    int ooff[NT][2];  // its offset r*J*I + i in the output tile
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        uint32_t r, i;
+        const uint32_t pos = p0 + nt * 8 + g;
+        P.I_div.divmod(pos, r, i);
+        okp[nt] = pos < slots;
+        base[nt] = okp[nt] ? (int)(r * KI + i) : 0;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const uint32_t pv = p0 + nt * 8 + 2 * t + v;
+            P.I_div.divmod(pv, r, i);
+            orow[nt][v] = pv < slots ? (int)r : -1;
+            ooff[nt][v] = (int)(r * J * I + i);
+        }
+    }
+    const double *brow = bsm + g * ldb + t;
+    const int Ki = (int)K, Ii = (int)I, Ji = (int)J;
+
+    for (int64_t q = 0; q < my_tiles; ++q) {
+        if (threadIdx.x == 0) bulk_wait_read<1>();  // outs[q & 1] is free (tile q-2 read out)
+        cp_async_wait<NST - 2>();
+        mbar_wait_parity(&full_bar[q % NST], (uint32_t)((q / NST) & 1));
+        __syncthreads();
+        if (q + NST - 1 < my_tiles) issue(q + NST - 1);
+        cp_async_commit();
+        const double *st = (const double *)(stages + (q % NST) * stage_bytes);
+        const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
+        const int rows = (int)(P.O - o0 < P.R ? P.O - o0 : P.R);
+
+        double acc[MT][NT][4];
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int b = 0; b < NT; ++b)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+        if (p0 < slots) {
+            for (int k4 = 0; k4 < Ki; k4 += 4) {
+                const int k = k4 + t;
+                const bool kok = k < Ki;
+                double bf[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) bf[nt] = (okp[nt] && kok) ? st[base[nt] + k * Ii] : 0.0;
+#pragma unroll
+                for (int mm = 0; mm < MT; ++mm) {
+                    const double a0 = brow[(mm * 16) * ldb + k4], a1 = brow[(mm * 16 + 8) * ldb + k4];
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
+                }
+            }
+            double *ot = outs + (q & 1) * (otile / 8);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    if (orow[nt][v] < 0 || orow[nt][v] >= rows) continue;
+#pragma unroll
+                    for (int mm = 0; mm < MT; ++mm)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int j = mm * 16 + g + 8 * h;
+                            if (j < Ji) ot[ooff[nt][v] + j * Ii] = acc[mm][nt][2 * h + v];
+                        }
+                }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = (uint32_t)(rows * J * I * 8);
+            const uint32_t b16 = bytes & ~15u;
+            const double *ot = outs + (q & 1) * (otile / 8);
+            double *dst = (double *)P.c + o0 * J * I;
+            if (b16) bulk_s2g(dst, ot, b16);
+            bulk_commit();
+            if (bytes != b16) dst[b16 / 8] = ot[b16 / 8];
+        }
+    }
+    cp_async_wait<0>();
+    if (threadIdx.x == 0) bulk_wait<0>();
+}
+
 static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                          int m0, TtmSimtParams &P) {
     const int64_t J = bm.extent[0];
@@ -337,6 +483,68 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
         return e ? atoi(e) : 4;
     }();
     static const bool force_simt = getenv("TL_TTM_SIMT") != nullptr;
+    static const int64_t bulk_kb = [] {
+        const char *e = getenv("TL_TTM_BULK_KB");
+        return (int64_t)(e ? atoi(e) : 14);
+    }();
+    static const int bulk_nt = [] {
+        const char *e = getenv("TL_TTM_BULK_NT");
+        return e ? atoi(e) : 2;
+    }();
+    static const int bulk_st = [] {
+        const char *e = getenv("TL_TTM_BULK_ST");
+        return e ? atoi(e) : 3;
+    }();
+    if (a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0 && bulk_kb > 0) {
+        // bulk-epilogue DMMA kernel: tiles of R slabs, outputs leave by TMA
+        const int nt = bulk_nt == 2 ? 2 : 4;
+        const int64_t rmax = std::max<int64_t>(1, std::min<int64_t>((64 * nt) / P.I, bulk_kb * 1024 / (KI * 8)));
+        // prefer R with R*I a multiple of the 8*nt positions one warp owns
+        // (no idle MMA columns), even if that overshoots the stage target
+        int64_t unit = 8 * nt;
+        for (int64_t d = P.I; d > 0;) {  // unit = 8 nt / gcd(I, 8 nt)
+            const int64_t r = unit % d;
+            unit = d;
+            d = r;
+        }
+        unit = 8 * nt / unit;
+        int64_t R = rmax / unit * unit;
+        if (R == 0 && unit * P.I <= 64 * nt && unit * KI * 8 <= 32 * 1024) R = unit;
+        if (R == 0) R = rmax;
+        while (R > 1 && ((R * KI * 8) % 16 != 0 || (R * P.J * P.I) % 2 != 0)) --R;
+        if ((R * KI * 8) % 16 == 0 && (R * P.J * P.I) % 2 == 0) {
+            P.R = (int32_t)R;
+            P.ntiles = (P.O + R - 1) / R;
+            P.I_div.init((uint32_t)P.I);
+            const int threads = (int)(((R * P.I + 8 * nt - 1) / (8 * nt)) * 32);
+            const size_t stage_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
+            const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
+            const int nst = bulk_st <= 3 ? 3 : (bulk_st <= 4 ? 4 : 6);
+            const size_t smem = StagedLayout<double, true>(P.J, P.K).bbytes + nst * stage_bytes + 2 * otile;
+            const DeviceInfo &di = device_info();
+            const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (228 * 1024) / (int64_t)(smem + 2048)));
+            const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * per_sm);
+            auto go = [&](auto kern) -> int {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return cuda_status(e, "ttm bulk smem");
+                kern<<<(unsigned)grid, threads, smem, st>>>(P);
+                return cuda_status(cudaGetLastError(), "ttm bulk launch");
+            };
+            if (smem <= 200 * 1024) {
+                auto pick = [&](auto mt, auto ntc) -> int {
+                    constexpr int MTv = decltype(mt)::value, NTv = decltype(ntc)::value;
+                    if (nst == 3) return go(ttm_bulk_kernel<MTv, NTv, 3>);
+                    if (nst == 4) return go(ttm_bulk_kernel<MTv, NTv, 4>);
+                    return go(ttm_bulk_kernel<MTv, NTv, 6>);
+                };
+                using I1 = std::integral_constant<int, 1>;
+                using I2 = std::integral_constant<int, 2>;
+                using I4 = std::integral_constant<int, 4>;
+                if (nt == 2) return P.J <= 16 ? pick(I1{}, I2{}) : pick(I2{}, I2{});
+                return P.J <= 16 ? pick(I1{}, I4{}) : pick(I2{}, I4{});
+            }
+        }
+    }
     const int64_t stage_target = stage_kb * 1024;
     int64_t R = std::max<int64_t>(1, std::min<int64_t>(256 / P.I, stage_target / (KI * s)));
     // keep every tile's start 16-byte aligned for the bulk copy

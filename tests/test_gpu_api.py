@@ -101,6 +101,11 @@ def ttm_case(shape, layout, mode, J, blayout, dtype, seed):
     ((12, 40, 10), (2, 3, 1), 2, 24, (2, 1)),   # staged DMMA (J = 24: two m-tiles)
     ((7, 9, 11), (3, 1, 2), 3, 5, (1, 2)),      # tiny J
     ((64, 8, 64), (1, 2, 3), 2, 200, (1, 2)),   # K < 16 -> exact fold path
+    ((5, 37, 2001), (1, 2, 3), 2, 32, (1, 2)),  # bulk-epilogue DMMA, J = 32 (two m-tiles)
+    ((5, 37, 2001), (1, 2, 3), 2, 7, (2, 1)),   # bulk-epilogue DMMA, odd J, odd tail tile
+    ((3, 33, 5, 17, 2, 64), (1, 2, 3, 4, 5, 6), 2, 16, (1, 2)),  # config-5 ttm shape (smaller)
+    ((9, 300, 41), (1, 2, 3), 2, 32, (1, 2)),   # J = 32, K large: B image too big -> GETT
+    ((200, 60, 3), (2, 1, 3), 1, 32, (1, 2)),   # J = 32 permuted output: staged direct stores
 ])
 def test_ttm_float64_paths(gpu, case):
     shape, layout, mode, J, blayout = case

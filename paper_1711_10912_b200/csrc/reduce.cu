@@ -34,6 +34,9 @@
 namespace tl {
 
 constexpr int kMaxPartials = 148 * 8;
+// longest FMA chain per binary64 partial of a sum of squares: relative error
+// <= (kFmaChain + log2(partials)) * 2^-53 < 5e-13
+constexpr int64_t kFmaChain = 4096;
 
 struct DD {  // double-double accumulator
     double hi, lo;
@@ -183,7 +186,10 @@ template <class TA> struct ThreadAcc {
     __device__ void add(int j, double x, double y) { dd_add_prod(dd[j & 1], x, y); }
     __device__ DD total() const { return dd_merge(dd[0], dd[1]); }
 };
-template <> struct ThreadAcc<float> {
+// FMA accumulation into 4 binary64 partials: exact products for float32;
+// for float64 sums of squares (the norm) when every partial folds at most
+// kFmaChain terms, so the blocked-sum bound (L + log2 P) eps stays < 1e-12.
+struct FmaAcc {
     double s[4];
     __device__ void zero() { s[0] = s[1] = s[2] = s[3] = 0.0; }
     __device__ void add(int j, double x, double y) { s[j & 3] = fma(x, y, s[j & 3]); }
@@ -195,6 +201,7 @@ template <> struct ThreadAcc<float> {
         return r;
     }
 };
+template <> struct ThreadAcc<float> : FmaAcc {};
 template <> struct ThreadAcc<int64_t> {
     Acc64 a;
     __device__ void zero() { a.v = 0; }
@@ -211,10 +218,10 @@ template <class T, int VEC> __device__ __forceinline__ void load_vec(const T *p,
     }
 }
 
-template <class TA, class TB, int VEC, bool SAME>
+template <class TA, class TB, int VEC, bool SAME, int U = 4, bool FMA_ACC = false>
 __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ ReduceParams P) {
     using Acc = typename RedAcc<TA>::type;
-    ThreadAcc<TA> ta;
+    typename std::conditional<FMA_ACC, FmaAcc, ThreadAcc<TA>>::type ta;
     ta.zero();
     const TA *a = (const TA *)P.a;
     const TB *b = (const TB *)P.b;
@@ -222,8 +229,7 @@ __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ R
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (P.n_rows == 1) {
-        // flat: 128-bit streaming loads, 4 vectors in flight per thread
-        constexpr int U = 4;
+        // flat: 128-bit streaming loads, U vectors in flight per thread
         const int64_t nv = L / VEC;
         int64_t v = tid;
         for (; v + (U - 1) * nthreads < nv; v += U * nthreads) {
@@ -239,9 +245,9 @@ __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ R
 #pragma unroll
                 for (int j = 0; j < VEC; ++j) {
                     if constexpr (SAME)
-                        ta.add(j, as_acc(xa[u][j]), as_acc(xa[u][j]));
+                        ta.add(u * VEC + j, as_acc(xa[u][j]), as_acc(xa[u][j]));
                     else
-                        ta.add(j, as_acc(xa[u][j]), as_acc(xb[u][j]));
+                        ta.add(u * VEC + j, as_acc(xa[u][j]), as_acc(xb[u][j]));
                 }
         }
         for (; v < nv; v += nthreads) {
@@ -612,7 +618,10 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
             else if (al) dot_rows_kernel<float, float, 4, false><<<G, threads, 0, st>>>(P);
             else dot_rows_kernel<float, float, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F64 && b.dtype == TL_F64) {
-            if (same && al) dot_rows_kernel<double, double, 2, true><<<G, threads, 0, st>>>(P);
+            // sum of squares: plain FMA partials when each folds <= kFmaChain terms
+            const bool fma_ok = (N + (int64_t)G * threads * 4 - 1) / ((int64_t)G * threads * 4) <= kFmaChain;
+            if (same && al && fma_ok) dot_rows_kernel<double, double, 2, true, 8, true><<<G, threads, 0, st>>>(P);
+            else if (same && al) dot_rows_kernel<double, double, 2, true, 8><<<G, threads, 0, st>>>(P);
             else if (al) dot_rows_kernel<double, double, 2, false><<<G, threads, 0, st>>>(P);
             else dot_rows_kernel<double, double, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F32 && b.dtype == TL_F64) {

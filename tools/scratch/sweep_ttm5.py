@@ -24,17 +24,21 @@ def timeit(fn, n=20):
         best = min(best, s.elapsed_time(e) / n * 1e3)
     return best
 
-out = {}
-T, v, M, layout = W.cfg5(0)
-A5 = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, layout), layout=layout)
-C1 = tl.ttv(A5, tl.DenseTensor.from_memory((9,), v), 5)
-Bm = tl.DenseTensor.from_memory(M.shape, W.layout_buffer(M, (1, 2)))
-C2 = tl.ttm(C1, Bm, 2)
-out["cfg5_ttm_us"] = round(timeit(lambda: tl.ttm(C1, Bm, 2)), 2)
-out["sha"] = __import__("hashlib").sha256(C2.numpy().tobytes()).hexdigest()[:16]
-rng = np.random.default_rng(1)
-X = tl.DenseTensor.from_memory((5, 37, 20001), rng.standard_normal((5, 37, 20001)).reshape(-1, order="F"))
-for J in (7, 16, 24, 32):
-    Mx = tl.DenseTensor.from_memory((J, 37), rng.standard_normal((J, 37)).reshape(-1, order="F"))
-    out[f"odd_J{J}_us"] = round(timeit(lambda: tl.ttm(X, Mx, 2)), 2)
-print(json.dumps(out))
+def main():
+    out = {}
+    T, v, M, layout = W.cfg5(0)
+    A5 = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, layout), layout=layout)
+    C1 = tl.ttv(A5, tl.DenseTensor.from_memory((9,), v), 5)
+    Bm = tl.DenseTensor.from_memory(M.shape, W.layout_buffer(M, (1, 2)))
+    C2 = tl.ttm(C1, Bm, 2)
+    out["cfg5_ttm_us"] = round(timeit(lambda: tl.ttm(C1, Bm, 2)), 2)
+    out["sha"] = __import__("hashlib").sha256(C2.numpy().tobytes()).hexdigest()[:16]
+    rng = np.random.default_rng(1)
+    X = tl.DenseTensor.from_memory((5, 37, 20001), rng.standard_normal((5, 37, 20001)).reshape(-1, order="F"))
+    for J in (7, 16, 24, 32):
+        Mx = tl.DenseTensor.from_memory((J, 37), rng.standard_normal((J, 37)).reshape(-1, order="F"))
+        out[f"odd_J{J}_us"] = round(timeit(lambda: tl.ttm(X, Mx, 2)), 2)
+    print(json.dumps(out))
+
+if __name__ == "__main__":
+    main()

@@ -52,6 +52,13 @@ struct TtvParams {
     FastDiv I_div;    // divides output slot j -> (row, i)
     FastDiv pr_div;   // pieces per row, full slab
     FastDiv pr_tail;  // pieces per row, last slab
+    // regime S, permuted outputs: out_map(o) = otab[o % E] + out_hi(o / E),
+    // otab (int32, shared memory) holding the map of the first otab_d0 digits
+    int32_t in_vec_ok;  // regime B: first inner digit's extent is a multiple of VEC
+    int32_t otab_n;   // E (0: plain digit map)
+    int32_t otab_d0;
+    FastDiv otab_div;
+    DigitMap out_hi;
 };
 
 // ------------------------------------------------------------- regime B
@@ -106,8 +113,15 @@ __device__ __forceinline__ void store_outputs(const TtvParams &P, int64_t o, int
         }
     } else {
         const int64_t go = P.out_map.map((uint32_t)o);
+        if (VEC > 1 && P.in_vec_ok) {
+            // i0 .. i0+VEC-1 share every inner digit but the first
+            const int64_t g0 = go + P.in_map.map((uint32_t)i0);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) c[go + P.in_map.map((uint32_t)(i0 + j))] = narrow<TC>(acc[j]);
+            for (int j = 0; j < VEC; ++j) c[g0 + j * P.in_map.stride[0]] = narrow<TC>(acc[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) c[go + P.in_map.map((uint32_t)(i0 + j))] = narrow<TC>(acc[j]);
+        }
     }
 }
 
@@ -346,8 +360,20 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
 
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
         bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
-    if constexpr (BULK) {
-        if (threadIdx.x == 0) {
+    int32_t *otab = (int32_t *)(stages + kStages * stage_bytes);
+    for (int w = threadIdx.x; w < P.otab_n; w += blockDim.x) {
+        uint32_t x = (uint32_t)w;
+        int64_t off = 0;
+        for (int d = 0; d < P.otab_d0; ++d) {
+            uint32_t q, r;
+            P.out_map.div[d].divmod(x, q, r);
+            off += (int64_t)r * P.out_map.stride[d];
+            x = q;
+        }
+        otab[w] = (int32_t)off;
+    }
+    if (BULK || P.otab_n) {
+        if (BULK && threadIdx.x == 0) {
             for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
             mbar_fence_init();
         }
@@ -446,10 +472,15 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
                     if (r < rows) {
                         const int64_t o = o0 + r;
                         int64_t off;
-                        if (P.ident)
+                        if (P.ident) {
                             off = o * I + i;
-                        else
+                        } else if (P.otab_n) {
+                            uint32_t qh, w;
+                            P.otab_div.divmod((uint32_t)o, qh, w);
+                            off = otab[w] + P.out_hi.map(qh) + P.in_map.map(i);
+                        } else {
                             off = P.out_map.map((uint32_t)o) + P.in_map.map(i);
+                        }
                         c[off] = narrow<TC>(acc[t]);
                     }
                 }
@@ -575,6 +606,7 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
     int threads = 256;
     while (threads > 32 && (nthreads + threads - 1) / threads < 2 * nsm) threads /= 2;
     P.b_smem = (P.K <= 8192) ? 1 : 0;
+    P.in_vec_ok = (P.in_map.n >= 1 && P.in_map.div[0].d % (uint32_t)vec == 0) ? 1 : 0;
     L.regime = 0;
     L.vec = vec;
     L.block = dim3(threads);
@@ -653,6 +685,8 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
     P.K = cn.K;
     P.I = cn.I;
     P.ident = cn.ident ? 1 : 0;
+    P.otab_n = 0;
+    P.otab_d0 = 0;
     if (!build_map(cn.inner, P.in_map) || !build_map(cn.outer, P.out_map)) {
         set_error("ttv: extent exceeds 32-bit digit range");
         return TL_EUNSUPPORTED;
@@ -679,6 +713,22 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
         ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
     } else {
         ok = plan_staged(L, (int64_t)s, base, di.num_sms);
+        if (ok && !P.ident && cn.outer.size() >= 3 && P.O * P.I < 0x7fffffffll) {
+            // permuted output: look up the low output digits in a shared table
+            int64_t E = 1;
+            int d0 = 0;
+            while (d0 + 1 < (int)cn.outer.size() && E * cn.outer[d0].first <= 1024) E *= cn.outer[d0++].first;
+            if (d0 >= 2) {
+                DigitList hi(cn.outer.begin() + d0, cn.outer.end());
+                build_map(hi, P.out_hi);
+                P.otab_n = (int32_t)E;
+                P.otab_d0 = d0;
+                P.otab_div.init((uint32_t)E);
+                L.smem += (size_t)E * 4;
+                const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / ((int64_t)L.smem + 2048)));
+                L.grid = dim3((unsigned)std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * per_sm));
+            }
+        }
         if (!ok) ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
     }
     if (!ok) {

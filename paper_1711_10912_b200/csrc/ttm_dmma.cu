@@ -14,12 +14,12 @@
 //   * otherwise a 2-D box: 8 positions along A's fastest free digit x 16
 //     along the output's fastest free digit (64-byte load runs; each CTA
 //     writes whole 32-byte sectors of C).
-// CTA tile 128 (J) x 128 (free) x 32 (k), FP64 m16n8k4 MMAs, 3-stage
-// cp.async pipeline, operands in padded shared memory (pitch = 4 mod 16
-// doubles: conflict-free fragment loads), fragments double-buffered in
-// registers, epilogue writes straight to first-order C.  Two warp layouts:
-// 8 warps of 64x32 (Cfg8) or 16 warps of 32x32 (Cfg16, <= 128 registers,
-// twice the warps to hide the DMMA issue latency).
+// Default CTA tile 64 (J) x 64 (free) x 32 (k), 4 warps of 32x32, FP64
+// m16n8k4 MMAs, 2-stage cp.async pipeline, three CTAs per SM (table at
+// Tile1); operands in padded shared memory (pitch = 4 mod 16 doubles:
+// conflict-free fragment loads), fragments double-buffered in registers; the
+// epilogue stages the tile in shared memory in C order and writes whole
+// warp runs of first-order C.
 //
 // Numerics: DMMA accumulates k in order with fused multiply-adds (measured
 // on B200: DMMA.8x8x4 == 4 sequential FMAs), so results differ from the
@@ -29,32 +29,46 @@
 #include <cstdlib>
 #include <string>
 #include <vector>
+#include <type_traits>
 
 #include "plan.h"
 #include "tl_common.cuh"
 
 namespace tl {
 
-namespace gett {
-constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int NST = 3;
-constexpr int LDW = BN + 4;  // pitch of [k][n] / [k][m] tiles (doubles)
-constexpr int LDK = BK + 4;  // pitch of [n][k] / [m][k] tiles (doubles)
-constexpr int A_TILE = BK * LDW > BN * LDK ? BK * LDW : BN * LDK;  // doubles
-constexpr int B_TILE = BK * LDW > BM * LDK ? BK * LDW : BM * LDK;
-constexpr int CP = BN + 4;   // staged-epilogue row pitch (doubles; = 4 mod 16)
-constexpr size_t SMEM = (size_t)NST * (A_TILE + B_TILE) * 8 + (size_t)BN * 28;
-static_assert(BM * CP <= NST * (A_TILE + B_TILE), "staged C tile must fit the operand stages");
-}  // namespace gett
+// CTA tile BM (J) x BN (free positions) x BK (k), NST-stage pipeline
+template <int BM_, int BN_, int BK_, int NST_> struct GettTile {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, NST = NST_;
+    static constexpr int LDWA = BN + 4;  // pitch of the [k][n] A tile (doubles, = 4 mod 16)
+    static constexpr int LDWB = BM + 4;  // pitch of the [k][m] B tile
+    static constexpr int LDK = BK + 4;   // pitch of [n][k] / [m][k] tiles
+    static constexpr int A_TILE = BK * LDWA > BN * LDK ? BK * LDWA : BN * LDK;  // doubles
+    static constexpr int B_TILE = BK * LDWB > BM * LDK ? BK * LDWB : BM * LDK;
+    static constexpr int CP = BN + 4;    // staged-epilogue row pitch
+    static constexpr size_t SMEM = (size_t)NST * (A_TILE + B_TILE) * 8 + (size_t)BN * 28;
+    static_assert(BM * CP <= NST * (A_TILE + B_TILE), "staged C tile must fit the operand stages");
+};
+// Measured on cfg3 (TFLOP/s, 6 layout/mode cases): smaller CTAs, several
+// per SM, keep the DMMA pipe busier than one big CTA whose 16 warps stall
+// together at every k-tile barrier (prologue/epilogue of one CTA overlap the
+// main loop of the others):
+//   128x128x32, 3 stages, 1 CTA/SM, 16 warps      29.3-29.7
+//   128x64x32,  2 stages, 2 CTAs/SM, 8 warps       31.2-32.5
+//   64x64x16,   3 stages, 3 CTAs/SM, 4 warps       31.5-32.8
+//   64x64x32,   2 stages, 3 CTAs/SM, 4 warps       31.8-33.2   (default)
+using Tile1 = GettTile<128, 128, 32, 3>;
+using Tile4 = GettTile<128, 64, 32, 2>;
+using Tile9 = GettTile<64, 64, 32, 2>;
+using Tile10 = GettTile<64, 64, 16, 3>;
 
 // warp layout: WM x WN warps, each TM m16 tiles x TN n8 tiles
 template <int WM_, int WN_, int TM_, int TN_> struct GettCfg {
     static constexpr int WM = WM_, WN = WN_, TM = TM_, TN = TN_;
     static constexpr int THREADS = 32 * WM * WN;
-    static_assert(WM * TM * 16 == gett::BM && WN * TN * 8 == gett::BN, "tile mismatch");
 };
-using Cfg8 = GettCfg<2, 4, 4, 4>;
-using Cfg16 = GettCfg<4, 4, 2, 4>;
+using Cfg16 = GettCfg<4, 4, 2, 4>;  // Tile1: 16 warps of 32 x 32
+using Cfg8x = GettCfg<4, 2, 2, 4>;  // Tile4: 8 warps of 32 x 32
+using Cfg4y = GettCfg<2, 2, 2, 4>;  // Tile9/10: 4 warps of 32 x 32
 
 struct TtmParams {
     const double *a;
@@ -87,10 +101,14 @@ __device__ __forceinline__ void mma_16x8x4(double (&d)[4], const double (&a)[2],
                  : "d"(a[0]), "d"(a[1]), "d"(b));
 }
 
-template <class CFG, bool A_KMAJOR, bool B_KMAJOR, bool PAIRS>
-__global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_constant__ TtmParams P) {
-    using namespace gett;
+template <class CFG, class TL, bool A_KMAJOR, bool B_KMAJOR, bool PAIRS, int MINB>
+__global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __grid_constant__ TtmParams P) {
     constexpr int THREADS = CFG::THREADS, TM = CFG::TM, TN = CFG::TN, WN = CFG::WN;
+    constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, NST = TL::NST;
+    constexpr int LDWA = TL::LDWA, LDWB = TL::LDWB, LDK = TL::LDK, A_TILE = TL::A_TILE, B_TILE = TL::B_TILE;
+    constexpr int CP = TL::CP;
+    static_assert(CFG::WM * TM * 16 == BM && CFG::WN * TN * 8 == BN, "tile mismatch");
+    static_assert(THREADS >= BN && THREADS >= BM, "one load column per thread");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *As = (double *)smem_raw;                 // NST x A_TILE
     double *Bs = As + NST * A_TILE;                  // NST x B_TILE
@@ -153,7 +171,7 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
     // Per-thread load assignment, fixed for the whole tile.  K-major
     // operands: lanes walk k (fixed k column per thread); otherwise lanes
     // walk n/m (fixed column, k rows).  Base pointers are formed once.
-    constexpr int LPT = (BK * BN) / THREADS;
+    constexpr int LPTA = (BK * BN) / THREADS, LPTB = (BK * BM) / THREADS;
     const int a_kk0 = A_KMAJOR ? (tid & (BK - 1)) : (tid / BN);
     const int a_nn0 = A_KMAJOR ? (tid / BK) : (tid & (BN - 1));
     const int b_kk0 = B_KMAJOR ? (tid & (BK - 1)) : (tid / BM);
@@ -165,7 +183,7 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
 
     // 16-byte variant: pairs of elements adjacent in both global and shared
     // memory (along n / m for N-major, along k for K-major), half the LDGSTS
-    constexpr int LPT2 = LPT / 2;
+    constexpr int LPTA2 = LPTA / 2, LPTB2 = LPTB / 2;
     const int a_p0 = A_KMAJOR ? 2 * (tid & (BK / 2 - 1)) : 2 * (tid & (BN / 2 - 1));  // element index of pair
     const int a_q0 = A_KMAJOR ? tid / (BK / 2) : tid / (BN / 2);
     const int b_p0 = B_KMAJOR ? 2 * (tid & (BK / 2 - 1)) : 2 * (tid & (BM / 2 - 1));
@@ -177,7 +195,7 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
         double *bs = Bs + stage * B_TILE;
         if constexpr (PAIRS) {
 #pragma unroll
-            for (int s = 0; s < LPT2; ++s) {
+            for (int s = 0; s < LPTA2; ++s) {
                 if constexpr (A_KMAJOR) {  // pair (k, k+1) of column nn
                     const int nn = a_q0 + s * (THREADS / (BK / 2));
                     const int64_t k = k0 + a_p0;
@@ -187,11 +205,11 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
                     const int kk = a_q0 + s * (THREADS / (BN / 2));
                     const int64_t k = k0 + kk;
                     const bool ok = (k < K) && (coff[a_p0] >= 0);
-                    cp_async16_zfill(as + kk * LDW + a_p0, P.a + (ok ? aoff[a_p0] + k * I : 0), ok);
+                    cp_async16_zfill(as + kk * LDWA + a_p0, P.a + (ok ? aoff[a_p0] + k * I : 0), ok);
                 }
             }
 #pragma unroll
-            for (int s = 0; s < LPT2; ++s) {
+            for (int s = 0; s < LPTB2; ++s) {
                 if constexpr (B_KMAJOR) {
                     const int mm = b_q0 + s * (THREADS / (BK / 2));
                     const int64_t k = k0 + b_p0, j = m0 + mm;
@@ -201,12 +219,12 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
                     const int kk = b_q0 + s * (THREADS / (BM / 2));
                     const int64_t k = k0 + kk, j = m0 + b_p0;
                     const bool ok = (k < K) && (j < P.J);
-                    cp_async16_zfill(bs + kk * LDW + b_p0, P.b + (ok ? j + k * P.bs1 : 0), ok);
+                    cp_async16_zfill(bs + kk * LDWB + b_p0, P.b + (ok ? j + k * P.bs1 : 0), ok);
                 }
             }
         } else {
 #pragma unroll
-            for (int s = 0; s < LPT; ++s) {
+            for (int s = 0; s < LPTA; ++s) {
                 if constexpr (A_KMAJOR) {
                     const int nn = a_nn0 + s * (THREADS / BK);
                     const int64_t k = k0 + a_kk0;
@@ -216,11 +234,11 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
                     const int kk = a_kk0 + s * (THREADS / BN);
                     const int64_t k = k0 + kk;
                     const bool ok = a_col_ok && (k < K);
-                    cp_async8_zfill(as + kk * LDW + a_nn0, ok ? a_base_fixed + k * I : P.a, ok);
+                    cp_async8_zfill(as + kk * LDWA + a_nn0, ok ? a_base_fixed + k * I : P.a, ok);
                 }
             }
 #pragma unroll
-            for (int s = 0; s < LPT; ++s) {
+            for (int s = 0; s < LPTB; ++s) {
                 if constexpr (B_KMAJOR) {
                     const int mm = b_mm0 + s * (THREADS / BK);
                     const int64_t k = k0 + b_kk0, j = m0 + mm;
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
                     const int kk = b_kk0 + s * (THREADS / BM);
                     const int64_t k = k0 + kk;
                     const bool ok = b_row_ok && (k < K);
-                    cp_async8_zfill(bs + kk * LDW + b_mm0, ok ? b_base_fixed + k * P.bs1 : P.b, ok);
+                    cp_async8_zfill(bs + kk * LDWB + b_mm0, ok ? b_base_fixed + k * P.bs1 : P.b, ok);
                 }
             }
         }
@@ -271,14 +289,14 @@ __global__ void __launch_bounds__(CFG::THREADS, 1) ttm_dmma_kernel(const __grid_
                     af[buf][i][0] = bs[m * LDK + k4 + t];
                     af[buf][i][1] = bs[(m + 8) * LDK + k4 + t];
                 } else {
-                    af[buf][i][0] = bs[(k4 + t) * LDW + m];
-                    af[buf][i][1] = bs[(k4 + t) * LDW + m + 8];
+                    af[buf][i][0] = bs[(k4 + t) * LDWB + m];
+                    af[buf][i][1] = bs[(k4 + t) * LDWB + m + 8];
                 }
             }
 #pragma unroll
             for (int j = 0; j < TN; ++j) {
                 const int n = wn * (8 * TN) + j * 8 + g;
-                bf[buf][j] = A_KMAJOR ? as[n * LDK + k4 + t] : as[(k4 + t) * LDW + n];
+                bf[buf][j] = A_KMAJOR ? as[n * LDK + k4 + t] : as[(k4 + t) * LDWA + n];
             }
         };
         load_frags(0, 0);
@@ -374,7 +392,14 @@ int ttm_dmma_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &
 
 static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
                     cudaStream_t st, std::string *describe) {
-    using namespace gett;
+    // CTA tile (see the table above Tile1); TL_GETT_TILE = 1, 4, 9 or 10
+    static const int tile_kind = [] {
+        const char *e = getenv("TL_GETT_TILE");
+        const int k = e ? atoi(e) : 9;
+        return (k == 1 || k == 4 || k == 10) ? k : 9;
+    }();
+    const int BM = tile_kind >= 9 ? 64 : 128;
+    const int BN = tile_kind == 1 ? 128 : 64;
     const int64_t J = bm.extent[0];
     Canon cn;
     if (!canon_contraction(a, m0, J, cn)) {
@@ -433,12 +458,12 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     if (sigma.size() > TL_MAX_DIGITS + 1) return TL_EUNSUPPORTED;
     int32_t box_a = 0, box_c = 0, box_s = 0;
     if (box) {
+        // store order inside one tile: the tile holds box_a A-fast x box_c C-fast positions
         box_a = (int32_t)sigma[0].ext;
-        box_c = (int32_t)sigma[1].ext;
+        box_c = (int32_t)std::min<int64_t>(sigma[1].ext, BN / std::max<int32_t>(1, box_a));
         box_s = box_a * box_c;
-        if (BN % box_s != 0) box_a = box_c = box_s = 0;
+        if (box_s == 0 || BN % box_s != 0 || sigma[1].ext % box_c != 0) box_a = box_c = box_s = 0;
     }
-
     TtmParams P{};
     P.a = (const double *)a_ptr + a.offset;
     P.b = (const double *)b_ptr + bm.offset;
@@ -491,18 +516,33 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         *describe = buf;
         return TL_OK;
     }
-    auto go = [&](auto kern) -> int {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        if (e != cudaSuccess) return cuda_status(e, "ttm smem attribute");
-        kern<<<(unsigned)grid, Cfg16::THREADS, SMEM, st>>>(P);
-        return cuda_status(cudaGetLastError(), "ttm dmma launch");
+    auto launch = [&](auto cfg, auto tl_, auto minb) -> int {
+        using CFG = decltype(cfg);
+        using TL = decltype(tl_);
+        constexpr int MINB = decltype(minb)::value;
+        auto go = [&](auto kern) -> int {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL::SMEM);
+            if (e != cudaSuccess) return cuda_status(e, "ttm smem attribute");
+            kern<<<(unsigned)grid, CFG::THREADS, TL::SMEM, st>>>(P);
+            return cuda_status(cudaGetLastError(), "ttm dmma launch");
+        };
+        if (pairs) {
+            if (a_kmajor)
+                return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, true, true, true, MINB>)
+                                : go(ttm_dmma_kernel<CFG, TL, true, false, true, MINB>);
+            return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, false, true, true, MINB>)
+                            : go(ttm_dmma_kernel<CFG, TL, false, false, true, MINB>);
+        }
+        if (a_kmajor)
+            return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, true, true, false, MINB>)
+                            : go(ttm_dmma_kernel<CFG, TL, true, false, false, MINB>);
+        return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, false, true, false, MINB>)
+                        : go(ttm_dmma_kernel<CFG, TL, false, false, false, MINB>);
     };
-    if (pairs) {
-        if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg16, true, true, true>) : go(ttm_dmma_kernel<Cfg16, true, false, true>);
-        return b_kmajor ? go(ttm_dmma_kernel<Cfg16, false, true, true>) : go(ttm_dmma_kernel<Cfg16, false, false, true>);
-    }
-    if (a_kmajor) return b_kmajor ? go(ttm_dmma_kernel<Cfg16, true, true, false>) : go(ttm_dmma_kernel<Cfg16, true, false, false>);
-    return b_kmajor ? go(ttm_dmma_kernel<Cfg16, false, true, false>) : go(ttm_dmma_kernel<Cfg16, false, false, false>);
+    if (tile_kind == 1) return launch(Cfg16{}, Tile1{}, std::integral_constant<int, 1>{});
+    if (tile_kind == 4) return launch(Cfg8x{}, Tile4{}, std::integral_constant<int, 2>{});
+    if (tile_kind == 10) return launch(Cfg4y{}, Tile10{}, std::integral_constant<int, 3>{});
+    return launch(Cfg4y{}, Tile9{}, std::integral_constant<int, 3>{});
 }
 
 }  // namespace tl

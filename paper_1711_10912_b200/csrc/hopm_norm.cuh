@@ -36,14 +36,28 @@ struct FusedNorm {
 __device__ __forceinline__ void hopm_normalize_block(const double *w, const FusedNorm &f, double *stage) {
     __shared__ double nrm;
     const int64_t n = f.n;
+    double *sq = stage != nullptr ? stage + n : nullptr;
     if (stage != nullptr) {
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) stage[i] = __ldcg(w + i);
+        // every thread squares its share (the products of the reference's
+        // fold, rounded identically); thread 0 then only runs the add chain
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const double x = __ldcg(w + i);
+            stage[i] = x;
+            sq[i] = __dmul_rn(x, x);
+        }
         __syncthreads();
     }
     if (threadIdx.x == 0) {
         double acc = 0.0;
         if (stage != nullptr) {
-            for (int64_t i = 0; i < n; ++i) acc = fold_step(acc, stage[i], stage[i]);
+            // blocks of 32 with a compile-time trip count: the loads issue
+            // ahead of the serial add chain
+            int64_t i = 0;
+            for (; i + 32 <= n; i += 32) {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) acc = __dadd_rn(acc, sq[i + q]);
+            }
+            for (; i < n; ++i) acc = __dadd_rn(acc, sq[i]);
         } else {
             for (int64_t i = 0; i < n; ++i) {
                 const double x = __ldcg(w + i);

@@ -217,7 +217,6 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
         for (int s = 0; s < nslab; ++s) mbar_init(&bars[s], blockDim.x);
         mbar_fence_init();
     }
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
     __syncthreads();
     if (threadIdx.x >= 32) {
         // warps 1..3 put the whole block in flight; warp 0 only folds
@@ -242,6 +241,9 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
             cp_async_mbar_arrive(&bars[s]);
         }
     } else {
+        // warp 0 stages b while the block's copies are in flight
+        for (int64_t k = threadIdx.x; k < K; k += 32) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+        __syncwarp();
         const int j = threadIdx.x;
         Acc acc = Acc(0);
         for (int s = 0; s < nslab; ++s) cp_async_mbar_arrive(&bars[s]);  // warp 0 issues no copies
@@ -249,26 +251,49 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
             mbar_wait_parity(&bars[s], 0);
             const int k0 = s * kSmallSlab;
             const int kn = (int)((K - k0) < kSmallSlab ? (K - k0) : kSmallSlab);
+            // A full slab is folded with its trip count known at compile
+            // time, so every shared-memory load is issued ahead of the
+            // dependent add chain (the fold's only serial part).
             if constexpr (ROWS) {
                 const TA *row = data + j * pitch + k0;
                 if constexpr (PAIRS) {
-                    int kk = 0;
+                    if (kn == kSmallSlab) {
+#pragma unroll
+                        for (int kk = 0; kk < kSmallSlab; kk += 2) {
+                            const double2 v = *(const double2 *)(row + kk);
+                            const double2 bv = *(const double2 *)(bs + k0 + kk);
+                            acc = fold_step(acc, (Acc)v.x, bv.x);
+                            acc = fold_step(acc, (Acc)v.y, bv.y);
+                        }
+                    } else {
+                        int kk = 0;
 #pragma unroll 4
-                    for (; kk + 1 < kn; kk += 2) {
-                        const double2 v = *(const double2 *)(row + kk);
-                        const double2 bv = *(const double2 *)(bs + k0 + kk);
-                        acc = fold_step(acc, (Acc)v.x, bv.x);
-                        acc = fold_step(acc, (Acc)v.y, bv.y);
+                        for (; kk + 1 < kn; kk += 2) {
+                            const double2 v = *(const double2 *)(row + kk);
+                            const double2 bv = *(const double2 *)(bs + k0 + kk);
+                            acc = fold_step(acc, (Acc)v.x, bv.x);
+                            acc = fold_step(acc, (Acc)v.y, bv.y);
+                        }
+                        if (kk < kn) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
                     }
-                    if (kk < kn) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
                 } else {
+                    if (kn == kSmallSlab) {
+#pragma unroll
+                        for (int kk = 0; kk < kSmallSlab; ++kk) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
+                    } else {
 #pragma unroll 8
-                    for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
+                        for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)row[kk], bs[k0 + kk]);
+                    }
                 }
             } else {
                 const TA *col = data + k0 * 32 + j;
+                if (kn == kSmallSlab) {
+#pragma unroll
+                    for (int kk = 0; kk < kSmallSlab; ++kk) acc = fold_step(acc, (Acc)col[kk * 32], bs[k0 + kk]);
+                } else {
 #pragma unroll 8
-                for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)col[kk * 32], bs[k0 + kk]);
+                    for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)col[kk * 32], bs[k0 + kk]);
+                }
             }
         }
         if (j < nout) {
@@ -630,21 +655,6 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         kern<<<L.grid, L.block, L.smem, st>>>(L.P);
         return cudaGetLastError();
     }
-    if (L.regime == 0) {
-        constexpr int U = 8;
-        if constexpr (sizeof(TA) == 4) {
-            if (L.vec == 4) {
-                ttv_strided_kernel<TA, TC, 4, U><<<L.grid, L.block, L.smem, st>>>(L.P);
-                return cudaGetLastError();
-            }
-        }
-        if (L.vec == 2) {
-            ttv_strided_kernel<TA, TC, 2, U><<<L.grid, L.block, L.smem, st>>>(L.P);
-        } else {
-            ttv_strided_kernel<TA, TC, 1, U><<<L.grid, L.block, L.smem, st>>>(L.P);
-        }
-        return cudaGetLastError();
-    }
     auto go = [&](auto kern) -> cudaError_t {
         if (L.smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
@@ -653,6 +663,14 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         kern<<<L.grid, L.block, L.smem, st>>>(L.P);
         return cudaGetLastError();
     };
+    if (L.regime == 0) {
+        constexpr int U = 8;
+        if constexpr (sizeof(TA) == 4) {
+            if (L.vec == 4) return go(ttv_strided_kernel<TA, TC, 4, U>);
+        }
+        if (L.vec == 2) return go(ttv_strided_kernel<TA, TC, 2, U>);
+        return go(ttv_strided_kernel<TA, TC, 1, U>);
+    }
     if (L.bulk) {
         if (L.vecread) return go(ttv_staged_kernel<TA, TC, 16, true, true>);
         return go(ttv_staged_kernel<TA, TC, 16, false, true>);
@@ -777,9 +795,10 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     P.b_stride = b_stride;
     P.b_dtype = b_dtype;
     if (fn != nullptr && fn->enabled) {
-        // the last CTA stages w (= this ttv's output) in its shared memory
+        // the last CTA stages w (= this ttv's output) and its squares in
+        // its shared memory
         P.fn = *fn;
-        L.smem = std::max(L.smem, (size_t)fn->n * sizeof(double));
+        L.smem = std::max(L.smem, 2 * (size_t)fn->n * sizeof(double));
     }
     cudaError_t e;
     if (a.dtype == TL_F32 && c_dtype == TL_F32) e = launch_typed<float, float>(L, st);

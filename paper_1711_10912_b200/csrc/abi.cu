@@ -18,7 +18,7 @@ namespace tl {
 struct FusedNorm;
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
                 int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
-                const FusedNorm *fn);
+                const FusedNorm *fn, bool pdl);
 int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                      int m0, cudaStream_t st);
 int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
@@ -169,7 +169,7 @@ int tl_ttv(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_
     }
     const void *bp = (const unsigned char *)b_ptr + b->offset * (int64_t)dtype_size(b->dtype);
     return ttv_enqueue(*a, a_ptr, bp, b->dtype, b->stride[0], c->dtype, c_ptr, mode - 1, nullptr,
-                       (cudaStream_t)stream, nullptr);
+                       (cudaStream_t)stream, nullptr, false);
 }
 
 int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr, const tl_desc *c, void *c_ptr,

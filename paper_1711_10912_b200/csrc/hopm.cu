@@ -21,6 +21,7 @@
 // twice per sweep instead of p times.  The norm of each 1-D w is the
 // reference's sequential fold done by one thread; u = w / norm uses IEEE
 // division -- so lambda history and vectors match the reference bit for bit.
+#include <cstdlib>
 #include <vector>
 
 #include "hopm_norm.cuh"
@@ -31,9 +32,20 @@ namespace tl {
 
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
                 int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
-                const FusedNorm *fn);
+                const FusedNorm *fn, bool pdl);
 
-constexpr int kNormSmem = 6000;  // doubles staged in shared memory for the norm fold
+constexpr int kNormSmem = 6000;
+// Programmatic dependent launch between the chained ttv kernels of a sweep
+// (TL_HOPM_PDL=1).  Off by default: measured at 400^3 it is SLOWER inside the
+// captured graph (4,170 vs 5,290 sweeps/s with the release placed either at
+// kernel start or before the fused-norm tail).
+static bool hopm_pdl() {
+    static const bool on = [] {
+        const char *e = getenv("TL_HOPM_PDL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}  // doubles staged in shared memory for the norm fold
 
 // Source of w: a float64 buffer, or (order-1 hopm) the tensor itself.
 struct WSource {
@@ -245,7 +257,7 @@ int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, d
                         use_ping = !use_ping;
                     }
                     int rc = ttv_enqueue(cur, cur_ptr, u[k - 1], TL_F64, 1, TL_F64, out, k - 1, stop, st,
-                                         k == last_k ? &fn : nullptr);
+                                         k == last_k ? &fn : nullptr, hopm_pdl());
                     if (rc != TL_OK) return rc;
                     cur = first_order_desc(q, shp, TL_F64);
                     cur_ptr = out;

@@ -208,6 +208,14 @@ template <int N> __device__ __forceinline__ void bulk_wait() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Programmatic dependent launch (no-ops for a kernel launched without the
+// programmatic-serialization attribute): pdl_wait blocks until the previous
+// kernel in the stream has completed and its writes are visible;
+// pdl_release lets the next kernel start launching once every CTA of this
+// one has called it (or exited).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ bool stop_requested(const int32_t *stop) {
     return stop != nullptr && *(volatile const int32_t *)stop != 0;
 }

@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc *bs = (Acc *)smem_raw;
+    pdl_wait();
     if (stop_requested(P.stop)) return;
     const int64_t K = P.K, I = P.I;
     if (P.b_smem) {
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
         }
         store_outputs<TC, VEC>(P, o, i0, acc);
     }
+    pdl_release();  // the next kernel's launch overlaps this one's tail
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[kSmallMaxSlabs];
+    pdl_wait();
     if (stop_requested(P.stop)) return;
     const int64_t K = P.K, I = P.I;
     const int nslab = (int)((K + kSmallSlab - 1) / kSmallSlab);
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
         }
     }
     cp_async_wait<0>();
+    pdl_release();  // the next kernel's launch overlaps this one's tail
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
@@ -375,6 +379,7 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[kStages];
+    pdl_wait();
     if (stop_requested(P.stop)) return;
     const int64_t K = P.K, I = P.I;
     // b (as the accumulation type), then kStages row-padded stage buffers
@@ -522,6 +527,7 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
         }
     }
     cp_async_wait<0>();
+    pdl_release();  // the next kernel's launch overlaps this one's tail
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
@@ -533,6 +539,7 @@ struct TtvLaunch {
     int G;
     bool vecread;
     bool bulk;
+    bool pdl;  // programmatic dependent launch (HOPM chains)
     dim3 grid, block;
     size_t smem;
 };
@@ -641,6 +648,26 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
     return true;
 }
 
+// <<<>>> or, for programmatic dependent launch, cudaLaunchKernelEx
+template <class Kern>
+static cudaError_t launch_kernel(Kern kern, const TtvLaunch &L, cudaStream_t st) {
+    if (!L.pdl) {
+        kern<<<L.grid, L.block, L.smem, st>>>(L.P);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = L.grid;
+    cfg.blockDim = L.block;
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, L.P);
+}
+
 template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
     if (L.regime == 2 || L.regime == 3) {
@@ -652,16 +679,14 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
             if (e != cudaSuccess) return e;
         }
-        kern<<<L.grid, L.block, L.smem, st>>>(L.P);
-        return cudaGetLastError();
+        return launch_kernel(kern, L, st);
     }
     auto go = [&](auto kern) -> cudaError_t {
         if (L.smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
             if (e != cudaSuccess) return e;
         }
-        kern<<<L.grid, L.block, L.smem, st>>>(L.P);
-        return cudaGetLastError();
+        return launch_kernel(kern, L, st);
     };
     if (L.regime == 0) {
         constexpr int U = 8;
@@ -782,13 +807,14 @@ int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
 // flag and binary64 outputs for float32 storage).
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
                 int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
-                const FusedNorm *fn) {
+                const FusedNorm *fn, bool pdl) {
     TtvLaunch L{};
     Canon cn;
     int rc = ttv_make_plan(a, a_ptr, m0, L, cn);
     if (rc != TL_OK) return rc;
     TtvParams &P = L.P;
     if (P.O * P.I == 0) return TL_OK;
+    L.pdl = pdl;
     P.b = b_ptr;
     P.c = c_ptr;
     P.stop = stop;

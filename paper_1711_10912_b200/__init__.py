@@ -36,10 +36,14 @@ from .layout import (
     zero_indices,
 )
 from .tensor import DenseTensor, tensors_equal
+from .views import Range, TensorView, classify_view
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "Range",
+    "TensorView",
+    "classify_view",
     "ContractionSpec",
     "outer_product",
     "reduce_ttm_to_ttt",

@@ -20,6 +20,7 @@ import torch
 from . import _abi
 from .layout import TensorMeta
 from .tensor import DenseTensor, _copy
+from .views import as_dense_operand
 
 __all__ = [
     "ContractionSpec",
@@ -39,9 +40,8 @@ __all__ = [
 
 
 def _operand(x) -> DenseTensor:
-    if isinstance(x, DenseTensor):
-        return x
-    raise TypeError(f"expected a DenseTensor, got {type(x).__name__}")
+    """DenseTensor or TensorView operand (contraction.py:52-55) as a DenseTensor."""
+    return as_dense_operand(x)
 
 
 def _vector(b, expected_len: int, what: str) -> DenseTensor:

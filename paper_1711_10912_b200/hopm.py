@@ -19,6 +19,7 @@ import torch
 from . import _abi
 from .layout import TensorMeta
 from .tensor import DenseTensor
+from .views import as_dense_operand
 
 __all__ = ["DegenerateInputError", "HopmState", "hopm", "HopmRunner", "rank_one_compose", "residual"]
 
@@ -91,6 +92,7 @@ class HopmRunner:
                  track_residuals: bool = False):
         if max_sweeps < 1:
             raise ValueError("max_sweeps must be >= 1")
+        a = as_dense_operand(a)
         if a.dtype not in (torch.float32, torch.float64):
             raise NotImplementedError("hopm requires floating elements")
         self.a = a
@@ -190,6 +192,7 @@ def rank_one_compose(scale: float, vectors: Sequence) -> DenseTensor:
 
 def residual(a, state: HopmState) -> float:
     """||a - rank_one_compose(state.scale, state.u)||_F (hopm.py:142-147)."""
+    a = as_dense_operand(a)
     vs, ptrs = _vector_ptrs(state.u, a.device)
     sc = torch.tensor([float(state.l[-1])], dtype=torch.float64, device=a.device)
     res = torch.empty(1, dtype=torch.float64, device=a.device)

@@ -283,9 +283,13 @@ def _copy(adesc, abuf: torch.Tensor, cdesc, cbuf: torch.Tensor) -> None:
 
 def tensors_equal(a, b) -> bool:
     """Equal order, shape and elements per zero-based multi-index; layout
-    and offsets are ignored (tensor.py:287-304)."""
+    and offsets are ignored; tensors and views alike (tensor.py:287-304)."""
     if a.order != b.order or a.shape != b.shape:
         return False
+    if not isinstance(a, DenseTensor) or not isinstance(b, DenseTensor):
+        from .views import as_dense_operand
+
+        a, b = as_dense_operand(a), as_dense_operand(b)
     if a.layout == b.layout:
         return bool(torch.equal(a.buffer, b.buffer.to(a.dtype)))
     tmp = torch.empty_like(b.buffer)

@@ -160,3 +160,39 @@ def test_meta_and_index_round_trip():
         TensorMeta((2, 0))
     with pytest.raises(ValueError):
         TensorMeta((2, 2), layout=(1, 1))
+
+
+def test_range_and_spec_validation_host():
+    """Host-side argument rules of views.py:25-80 and contraction.py:304-334,
+    421-440 (no device needed)."""
+    from paper_1711_10912_b200 import ContractionSpec, Range, reduce_ttm_to_ttt, reduce_ttv_to_ttt
+
+    assert Range().is_full
+    r = Range(2, 3, 9)
+    assert (r.first, r.step, r.last) == (2, 3, 9)
+    assert r.resolve(0, 10, 1) == (2, 3, 9)
+    assert Range(4).resolve(1, 5, 1) == (4, 1, 4)
+    for bad in [(3, 1), (1, 0, 4), (1, 2, 3, 4)]:
+        with pytest.raises(ValueError):
+            Range(*bad)
+    with pytest.raises(IndexError):
+        Range(0, 10).resolve(0, 10, 1)
+    s = ContractionSpec(2, [3, 1, 2], [3, 2, 1])
+    assert (s.q, s.r, s.s, s.phi, s.psi) == (2, 1, 1, (3, 1, 2), (3, 2, 1))
+    for bad in [(1, (1, 1), (1,)), (2, (1,), (1, 2)), (-1, (1,), (1,)), (0, (), (1,))]:
+        with pytest.raises(ValueError):
+            ContractionSpec(*bad)
+    assert reduce_ttv_to_ttt(3, 2) == ContractionSpec(1, (1, 3, 2), (1,))
+    assert reduce_ttm_to_ttt(4, 1) == ContractionSpec(1, (2, 3, 4, 1), (1, 2))
+    with pytest.raises(ValueError):
+        reduce_ttm_to_ttt(2, 0)
+
+
+def test_gett_tile_store_order():
+    # 64-wide tiles hold 8 A-fast x 8 C-fast positions of the 8 x 16 box; the
+    # staged epilogue writes them in C order
+    p = plan(1, (512,) * 3, (3, 2, 1), 2, _abi.TL_F64, (384, 512))
+    assert p["box"] == 64
+    assert plan(1, (512,) * 3, (1, 2, 3), 2, _abi.TL_F64, (384, 512))["box"] == 0
+    # J = 32 with a small K now stays on the staged kernels
+    assert plan(1, (5, 37, 2001), (1, 2, 3), 2, _abi.TL_F64, (32, 37))["path"] == "staged"

@@ -356,10 +356,16 @@ def components(args):
             tf[f"{lname}_q{mode}"] = round(2 * 512 ** 3 * 384 / (ms * 1e-3) / 1e12, 2)
         del A
         torch.cuda.empty_cache()
-    del A_
     out["cfg3_ttm_tflops"] = tf
     out["cfg3_ttm_tflops_min"] = min(tf.values())
     out["cfg3_ttm_frac_fp64_peak_min"] = round(min(tf.values()) / FP64_PEAK_TFLOPS, 3)
+    # the same shape in float32 storage (widened onto the FP64 tensor cores;
+    # an extension: the reference has no float32)
+    A32 = tl.DenseTensor.from_memory(A_.shape, W.layout_buffer(A_, (1, 2, 3)).astype(np.float32))
+    B32 = Bm.to(torch.float32)
+    ms = med_eager(lambda: tl.ttm(A32, B32, 2), iters=3, warm=1)
+    out["cfg3_f32_first_q2_tflops"] = round(2 * 512 ** 3 * 384 / (ms * 1e-3) / 1e12, 2)
+    del A32, B32, A_
     # config 4: HOPM
     T, _ = W.cfg4()
     A = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, (1, 2, 3)))

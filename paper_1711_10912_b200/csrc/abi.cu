@@ -210,14 +210,16 @@ int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void 
     }
     cudaStream_t st = (cudaStream_t)stream;
     // few rows J (<= 32): the staged tile kernels (HBM-bound; DMMA for
-    // float64); GEMM-shaped float64 -> DMMA GETT; anything else -> one
-    // thread per output
+    // float64); GEMM-shaped float64 or float32 -> DMMA GETT (float32 widened:
+    // its products are exact in binary64, so the FMA chain equals the
+    // reference's fold); anything else -> one thread per output
     const bool few_rows = bmat->extent[0] <= 32;
-    if (few_rows || a->dtype != TL_F64) {
+    const bool fp = a->dtype == TL_F64 || a->dtype == TL_F32;
+    if (few_rows || !fp) {
         int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
         if (rc != TL_EUNSUPPORTED) return rc;
     }
-    if (a->dtype == TL_F64) {
+    if (fp) {
         int rc = ttm_dmma_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
         if (rc != TL_EUNSUPPORTED) return rc;
         if (!few_rows) {

@@ -71,9 +71,9 @@ using Cfg8x = GettCfg<4, 2, 2, 4>;  // Tile4: 8 warps of 32 x 32
 using Cfg4y = GettCfg<2, 2, 2, 4>;  // Tile9/10: 4 warps of 32 x 32
 
 struct TtmParams {
-    const double *a;
-    const double *b;
-    double *c;
+    const void *a;  // TA elements (float64, or float32 widened exactly on the fragment loads)
+    const void *b;
+    void *c;
     int64_t J, K, I, F;
     int64_t jstride;
     int64_t bs0, bs1;
@@ -90,9 +90,23 @@ __device__ __forceinline__ void cp_async8_zfill(void *smem_dst, const void *gmem
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(n));
 }
 
+__device__ __forceinline__ void cp_async4_zfill(void *smem_dst, const void *gmem_src, bool valid) {
+    const int n = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(n));
+}
+
+
 __device__ __forceinline__ void cp_async16_zfill(void *smem_dst, const void *gmem_src, bool valid) {
     const int n = valid ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src), "r"(n));
+}
+
+// one element / an adjacent pair of TA elements, zero-filled when !valid
+template <class TA> __device__ __forceinline__ void cp_elem(void *d, const void *s, bool valid) {
+    if constexpr (sizeof(TA) == 8) cp_async8_zfill(d, s, valid); else cp_async4_zfill(d, s, valid);
+}
+template <class TA> __device__ __forceinline__ void cp_pair(void *d, const void *s, bool valid) {
+    if constexpr (sizeof(TA) == 8) cp_async16_zfill(d, s, valid); else cp_async8_zfill(d, s, valid);
 }
 
 __device__ __forceinline__ void mma_16x8x4(double (&d)[4], const double (&a)[2], double b) {
@@ -101,7 +115,7 @@ __device__ __forceinline__ void mma_16x8x4(double (&d)[4], const double (&a)[2],
                  : "d"(a[0]), "d"(a[1]), "d"(b));
 }
 
-template <class CFG, class TL, bool A_KMAJOR, bool B_KMAJOR, bool PAIRS, int MINB>
+template <class TA, class CFG, class TL, bool A_KMAJOR, bool B_KMAJOR, bool PAIRS, int MINB>
 __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __grid_constant__ TtmParams P) {
     constexpr int THREADS = CFG::THREADS, TM = CFG::TM, TN = CFG::TN, WN = CFG::WN;
     constexpr int BM = TL::BM, BN = TL::BN, BK = TL::BK, NST = TL::NST;
@@ -110,9 +124,13 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
     static_assert(CFG::WM * TM * 16 == BM && CFG::WN * TN * 8 == BN, "tile mismatch");
     static_assert(THREADS >= BN && THREADS >= BM, "one load column per thread");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *As = (double *)smem_raw;                 // NST x A_TILE
-    double *Bs = As + NST * A_TILE;                  // NST x B_TILE
-    int64_t *aoff = (int64_t *)(Bs + NST * B_TILE);  // BN
+    TA *As = (TA *)smem_raw;                         // NST x A_TILE
+    TA *Bs = As + NST * A_TILE;                      // NST x B_TILE
+    // tables after the (double-sized) operand area, which the epilogue reuses
+    int64_t *aoff = (int64_t *)(smem_raw + (size_t)NST * (A_TILE + B_TILE) * sizeof(double));  // BN
+    const TA *Pa = (const TA *)P.a;
+    const TA *Pb = (const TA *)P.b;
+    TA *Pc = (TA *)P.c;
     int64_t *coff = aoff + BN;                       // BN  (-1: masked column)
     int64_t *coffp = coff + BN;                      // BN  C offset of store position l
     int32_t *lpos = (int32_t *)(coffp + BN);         // BN  store position of column n
@@ -176,9 +194,9 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
     const int a_nn0 = A_KMAJOR ? (tid / BK) : (tid & (BN - 1));
     const int b_kk0 = B_KMAJOR ? (tid & (BK - 1)) : (tid / BM);
     const int b_mm0 = B_KMAJOR ? (tid / BK) : (tid & (BM - 1));
-    const double *a_base_fixed = P.a + aoff[a_nn0];
+    const TA *a_base_fixed = Pa + aoff[a_nn0];
     const bool a_col_ok = coff[a_nn0] >= 0;
-    const double *b_base_fixed = P.b + (m0 + b_mm0) * P.bs0;
+    const TA *b_base_fixed = Pb + (m0 + b_mm0) * P.bs0;
     const bool b_row_ok = (m0 + b_mm0) < P.J;
 
     // 16-byte variant: pairs of elements adjacent in both global and shared
@@ -191,8 +209,8 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
 
     auto load_stage = [&](int stage, int kt) {
         const int64_t k0 = (int64_t)kt * BK;
-        double *as = As + stage * A_TILE;
-        double *bs = Bs + stage * B_TILE;
+        TA *as = As + stage * A_TILE;
+        TA *bs = Bs + stage * B_TILE;
         if constexpr (PAIRS) {
 #pragma unroll
             for (int s = 0; s < LPTA2; ++s) {
@@ -200,12 +218,12 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
                     const int nn = a_q0 + s * (THREADS / (BK / 2));
                     const int64_t k = k0 + a_p0;
                     const bool ok = (k < K) && (coff[nn] >= 0);
-                    cp_async16_zfill(as + nn * LDK + a_p0, P.a + (ok ? aoff[nn] + k : 0), ok);
+                    cp_pair<TA>(as + nn * LDK + a_p0, Pa + (ok ? aoff[nn] + k : 0), ok);
                 } else {  // pair (n, n+1) of row kk
                     const int kk = a_q0 + s * (THREADS / (BN / 2));
                     const int64_t k = k0 + kk;
                     const bool ok = (k < K) && (coff[a_p0] >= 0);
-                    cp_async16_zfill(as + kk * LDWA + a_p0, P.a + (ok ? aoff[a_p0] + k * I : 0), ok);
+                    cp_pair<TA>(as + kk * LDWA + a_p0, Pa + (ok ? aoff[a_p0] + k * I : 0), ok);
                 }
             }
 #pragma unroll
@@ -214,12 +232,12 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
                     const int mm = b_q0 + s * (THREADS / (BK / 2));
                     const int64_t k = k0 + b_p0, j = m0 + mm;
                     const bool ok = (k < K) && (j < P.J);
-                    cp_async16_zfill(bs + mm * LDK + b_p0, P.b + (ok ? j * P.bs0 + k : 0), ok);
+                    cp_pair<TA>(bs + mm * LDK + b_p0, Pb + (ok ? j * P.bs0 + k : 0), ok);
                 } else {
                     const int kk = b_q0 + s * (THREADS / (BM / 2));
                     const int64_t k = k0 + kk, j = m0 + b_p0;
                     const bool ok = (k < K) && (j < P.J);
-                    cp_async16_zfill(bs + kk * LDWB + b_p0, P.b + (ok ? j + k * P.bs1 : 0), ok);
+                    cp_pair<TA>(bs + kk * LDWB + b_p0, Pb + (ok ? j + k * P.bs1 : 0), ok);
                 }
             }
         } else {
@@ -229,12 +247,12 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
                     const int nn = a_nn0 + s * (THREADS / BK);
                     const int64_t k = k0 + a_kk0;
                     const bool ok = (k < K) && (coff[nn] >= 0);
-                    cp_async8_zfill(as + nn * LDK + a_kk0, P.a + (ok ? aoff[nn] + k : 0), ok);
+                    cp_elem<TA>(as + nn * LDK + a_kk0, Pa + (ok ? aoff[nn] + k : 0), ok);
                 } else {
                     const int kk = a_kk0 + s * (THREADS / BN);
                     const int64_t k = k0 + kk;
                     const bool ok = a_col_ok && (k < K);
-                    cp_async8_zfill(as + kk * LDWA + a_nn0, ok ? a_base_fixed + k * I : P.a, ok);
+                    cp_elem<TA>(as + kk * LDWA + a_nn0, ok ? a_base_fixed + k * I : Pa, ok);
                 }
             }
 #pragma unroll
@@ -243,12 +261,12 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
                     const int mm = b_mm0 + s * (THREADS / BK);
                     const int64_t k = k0 + b_kk0, j = m0 + mm;
                     const bool ok = (k < K) && (j < P.J);
-                    cp_async8_zfill(bs + mm * LDK + b_kk0, P.b + (ok ? j * P.bs0 + k : 0), ok);
+                    cp_elem<TA>(bs + mm * LDK + b_kk0, Pb + (ok ? j * P.bs0 + k : 0), ok);
                 } else {
                     const int kk = b_kk0 + s * (THREADS / BM);
                     const int64_t k = k0 + kk;
                     const bool ok = b_row_ok && (k < K);
-                    cp_async8_zfill(bs + kk * LDWB + b_mm0, ok ? b_base_fixed + k * P.bs1 : P.b, ok);
+                    cp_elem<TA>(bs + kk * LDWB + b_mm0, ok ? b_base_fixed + k * P.bs1 : Pb, ok);
                 }
             }
         }
@@ -276,8 +294,8 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
             if (nk < KT) load_stage(nk % NST, nk);
             cp_async_commit();
         }
-        const double *as = As + (kt % NST) * A_TILE;
-        const double *bs = Bs + (kt % NST) * B_TILE;
+        const TA *as = As + (kt % NST) * A_TILE;
+        const TA *bs = Bs + (kt % NST) * B_TILE;
         // fragments double-buffered in registers: step k4+1 is loaded from
         // shared memory while step k4's MMAs issue
         double af[2][TM][2], bf[2][TN];
@@ -327,7 +345,7 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
                     for (int v = 0; v < 2; ++v) {
                         const int n = wn * (8 * TN) + jj * 8 + 2 * t + v;
                         const int64_t co = coff[n];
-                        if (co >= 0) P.c[co + j] = acc[i][jj][2 * h + v];
+                        if (co >= 0) Pc[co + j] = (TA)acc[i][jj][2 * h + v];
                     }
                 }
             }
@@ -338,7 +356,7 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
     // position l, skewed one double per 32 positions: 2 wavefronts per
     // access both ways) and write whole 256-byte warp runs of C.
     __syncthreads();  // every warp is done with the operand stages
-    double *cs = As;
+    double *cs = (double *)smem_raw;
     int ln[TN][2];
 #pragma unroll
     for (int jj = 0; jj < TN; ++jj)
@@ -366,7 +384,7 @@ __global__ void __launch_bounds__(CFG::THREADS, MINB) ttm_dmma_kernel(const __gr
 #pragma unroll 4
             for (int m = tid / BN; m < BM; m += THREADS / BN) {
                 const int64_t j = m0 + m;
-                if (j < P.J) P.c[co + j * P.jstride] = src[m * CP];
+                if (j < P.J) Pc[co + j * P.jstride] = (TA)src[m * CP];
             }
         }
     }
@@ -464,10 +482,16 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         box_s = box_a * box_c;
         if (box_s == 0 || BN % box_s != 0 || sigma[1].ext % box_c != 0) box_a = box_c = box_s = 0;
     }
+    // float64, or float32 widened exactly on the fragment loads (binary64
+    // accumulation, one rounding on store: within the float32 tolerance)
+    if (a.dtype != TL_F64 && a.dtype != TL_F32) return TL_EUNSUPPORTED;
+    const bool f32 = a.dtype == TL_F32;
+    const int64_t es = f32 ? 4 : 8;
+    if (f32 && tile_kind != 9) return TL_EUNSUPPORTED;
     TtmParams P{};
-    P.a = (const double *)a_ptr + a.offset;
-    P.b = (const double *)b_ptr + bm.offset;
-    P.c = (double *)c_ptr;
+    P.a = (const char *)a_ptr + a.offset * es;
+    P.b = (const char *)b_ptr + bm.offset * es;
+    P.c = c_ptr;
     P.J = J;
     P.K = cn.K;
     P.I = cn.I;
@@ -490,10 +514,10 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     const int64_t grid = ntiles * P.mtiles;
     if (grid > 0x7fffffffll) return TL_EUNSUPPORTED;
     const bool b_kmajor = (bm.stride[1] == 1 && bm.extent[1] > 1);
-    // 16-byte operand pairs: both elements of every pair adjacent in global
-    // memory, 16-byte aligned, and never straddling a masked column
+    // operand pairs (one 16-byte copy for float64, 8-byte for float32): both
+    // elements adjacent in global memory, aligned, never straddling a masked column
     const uintptr_t pa = (uintptr_t)P.a, pb = (uintptr_t)P.b;
-    bool pairs = (pa % 16 == 0) && (pb % 16 == 0);
+    bool pairs = (pa % (2 * es) == 0) && (pb % (2 * es) == 0);
     if (a_kmajor)
         pairs = pairs && (cn.K % 2 == 0);
     else
@@ -504,10 +528,11 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         pairs = pairs && (P.bs0 == 1) && (J % 2 == 0) && (P.bs1 % 2 == 0);
     if (describe != nullptr) {
         char buf[1024];
-        int n = snprintf(buf, sizeof(buf), "{\"path\": \"gett\", \"O\": %lld, \"K\": %lld, \"I\": %lld, \"J\": %lld, "
+        int n = snprintf(buf, sizeof(buf), "{\"path\": \"gett\", \"dtype\": \"%s\", \"O\": %lld, \"K\": %lld, \"I\": %lld, \"J\": %lld, "
                          "\"jstride\": %lld, \"a_kmajor\": %d, \"b_kmajor\": %d, \"pairs\": %d, \"grid\": %lld, \"box\": %d, "
                          "\"sigma\": [",
-                         (long long)cn.O, (long long)cn.K, (long long)cn.I, (long long)J, (long long)cn.jstride,
+                         f32 ? "f32" : "f64", (long long)cn.O, (long long)cn.K, (long long)cn.I, (long long)J,
+                         (long long)cn.jstride,
                          a_kmajor ? 1 : 0, b_kmajor ? 1 : 0, pairs ? 1 : 0, (long long)grid, (int)box_s);
         for (size_t d = 0; d < sigma.size() && n < (int)sizeof(buf) - 64; ++d)
             n += snprintf(buf + n, sizeof(buf) - n, "%s[%lld, %lld, %lld]", d ? ", " : "", (long long)sigma[d].ext,
@@ -516,7 +541,8 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         *describe = buf;
         return TL_OK;
     }
-    auto launch = [&](auto cfg, auto tl_, auto minb) -> int {
+    auto launch = [&](auto ta, auto cfg, auto tl_, auto minb) -> int {
+        using TA = decltype(ta);
         using CFG = decltype(cfg);
         using TL = decltype(tl_);
         constexpr int MINB = decltype(minb)::value;
@@ -528,21 +554,22 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
         };
         if (pairs) {
             if (a_kmajor)
-                return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, true, true, true, MINB>)
-                                : go(ttm_dmma_kernel<CFG, TL, true, false, true, MINB>);
-            return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, false, true, true, MINB>)
-                            : go(ttm_dmma_kernel<CFG, TL, false, false, true, MINB>);
+                return b_kmajor ? go(ttm_dmma_kernel<TA, CFG, TL, true, true, true, MINB>)
+                                : go(ttm_dmma_kernel<TA, CFG, TL, true, false, true, MINB>);
+            return b_kmajor ? go(ttm_dmma_kernel<TA, CFG, TL, false, true, true, MINB>)
+                            : go(ttm_dmma_kernel<TA, CFG, TL, false, false, true, MINB>);
         }
         if (a_kmajor)
-            return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, true, true, false, MINB>)
-                            : go(ttm_dmma_kernel<CFG, TL, true, false, false, MINB>);
-        return b_kmajor ? go(ttm_dmma_kernel<CFG, TL, false, true, false, MINB>)
-                        : go(ttm_dmma_kernel<CFG, TL, false, false, false, MINB>);
+            return b_kmajor ? go(ttm_dmma_kernel<TA, CFG, TL, true, true, false, MINB>)
+                            : go(ttm_dmma_kernel<TA, CFG, TL, true, false, false, MINB>);
+        return b_kmajor ? go(ttm_dmma_kernel<TA, CFG, TL, false, true, false, MINB>)
+                        : go(ttm_dmma_kernel<TA, CFG, TL, false, false, false, MINB>);
     };
-    if (tile_kind == 1) return launch(Cfg16{}, Tile1{}, std::integral_constant<int, 1>{});
-    if (tile_kind == 4) return launch(Cfg8x{}, Tile4{}, std::integral_constant<int, 2>{});
-    if (tile_kind == 10) return launch(Cfg4y{}, Tile10{}, std::integral_constant<int, 3>{});
-    return launch(Cfg4y{}, Tile9{}, std::integral_constant<int, 3>{});
+    if (f32) return launch(float{}, Cfg4y{}, Tile9{}, std::integral_constant<int, 3>{});
+    if (tile_kind == 1) return launch(double{}, Cfg16{}, Tile1{}, std::integral_constant<int, 1>{});
+    if (tile_kind == 4) return launch(double{}, Cfg8x{}, Tile4{}, std::integral_constant<int, 2>{});
+    if (tile_kind == 10) return launch(double{}, Cfg4y{}, Tile10{}, std::integral_constant<int, 3>{});
+    return launch(double{}, Cfg4y{}, Tile9{}, std::integral_constant<int, 3>{});
 }
 
 }  // namespace tl

@@ -125,6 +125,21 @@ def test_ttm_exact_dtypes(gpu, dtype):
         assert np.array_equal(bits(got), bits(want)), case
 
 
+@pytest.mark.parametrize("case", [
+    ((48, 40, 36), (1, 2, 3), 1, 64, (1, 2)),
+    ((48, 40, 36), (3, 2, 1), 2, 96, (2, 1)),
+    ((33, 70, 41), (2, 3, 1), 3, 40, (1, 2)),
+    ((3, 33, 5, 17, 2, 64), (1, 2, 3, 4, 5, 6), 2, 48, (1, 2)),
+])
+def test_ttm_float32_gett_bit_exact(gpu, case):
+    """float32 on the DMMA GETT: binary64 products of float32 values are
+    exact, so each FMA step equals the reference's mul-then-add and the
+    result, rounded once, is bit-identical."""
+    shape, layout, mode, J, blayout = case
+    got, want, _ = ttm_case(shape, layout, mode, J, blayout, "float32", 8)
+    assert np.array_equal(bits(got), bits(want.astype(np.float32))), case
+
+
 @pytest.mark.parametrize("q,layout", [(1, (1, 2, 3)), (2, (1, 2, 3)), (3, (1, 2, 3)),
                                       (1, (3, 2, 1)), (2, (3, 2, 1)), (3, (3, 2, 1))])
 def test_cfg3_ttm_full_size_sampled(gpu, q, layout):

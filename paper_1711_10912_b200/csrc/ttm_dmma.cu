@@ -60,6 +60,7 @@ using Tile1 = GettTile<128, 128, 32, 3>;
 using Tile4 = GettTile<128, 64, 32, 2>;
 using Tile9 = GettTile<64, 64, 32, 2>;
 using Tile10 = GettTile<64, 64, 16, 3>;
+using Tile12 = GettTile<64, 64, 16, 2>;
 
 // warp layout: WM x WN warps, each TM m16 tiles x TN n8 tiles
 template <int WM_, int WN_, int TM_, int TN_> struct GettCfg {
@@ -414,7 +415,7 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     static const int tile_kind = [] {
         const char *e = getenv("TL_GETT_TILE");
         const int k = e ? atoi(e) : 9;
-        return (k == 1 || k == 4 || k == 10) ? k : 9;
+        return (k == 1 || k == 4 || k == 10 || k == 12) ? k : 9;
     }();
     const int BM = tile_kind >= 9 ? 64 : 128;
     const int BN = tile_kind == 1 ? 128 : 64;
@@ -569,6 +570,7 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
     if (tile_kind == 1) return launch(double{}, Cfg16{}, Tile1{}, std::integral_constant<int, 1>{});
     if (tile_kind == 4) return launch(double{}, Cfg8x{}, Tile4{}, std::integral_constant<int, 2>{});
     if (tile_kind == 10) return launch(double{}, Cfg4y{}, Tile10{}, std::integral_constant<int, 3>{});
+    if (tile_kind == 12) return launch(double{}, Cfg4y{}, Tile12{}, std::integral_constant<int, 4>{});
     return launch(double{}, Cfg4y{}, Tile9{}, std::integral_constant<int, 3>{});
 }
 

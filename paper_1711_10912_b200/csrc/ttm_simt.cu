@@ -493,11 +493,11 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
     }();
     static const int bulk_st = [] {
         const char *e = getenv("TL_TTM_BULK_ST");
-        return e ? atoi(e) : 3;
+        return e ? atoi(e) : 2;  // measured: 2 stages (more CTAs per SM) beat 3-4
     }();
     if (a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0 && bulk_kb > 0) {
         // bulk-epilogue DMMA kernel: tiles of R slabs, outputs leave by TMA
-        const int nt = bulk_nt == 2 ? 2 : 4;
+        const int nt = (bulk_nt == 1 || bulk_nt == 4) ? bulk_nt : 2;
         const int64_t rmax = std::max<int64_t>(1, std::min<int64_t>((64 * nt) / P.I, bulk_kb * 1024 / (KI * 8)));
         // prefer R with R*I a multiple of the 8*nt positions one warp owns
         // (no idle MMA columns), even if that overshoots the stage target
@@ -519,7 +519,7 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
             const int threads = (int)(((R * P.I + 8 * nt - 1) / (8 * nt)) * 32);
             const size_t stage_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
             const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
-            const int nst = bulk_st <= 3 ? 3 : (bulk_st <= 4 ? 4 : 6);
+            const int nst = bulk_st <= 2 ? 2 : (bulk_st == 3 ? 3 : 4);
             const size_t smem = StagedLayout<double, true>(P.J, P.K).bbytes + nst * stage_bytes + 2 * otile;
             const DeviceInfo &di = device_info();
             const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (228 * 1024) / (int64_t)(smem + 2048)));
@@ -533,13 +533,14 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
             if (smem <= 200 * 1024) {
                 auto pick = [&](auto mt, auto ntc) -> int {
                     constexpr int MTv = decltype(mt)::value, NTv = decltype(ntc)::value;
+                    if (nst == 2) return go(ttm_bulk_kernel<MTv, NTv, 2>);
                     if (nst == 3) return go(ttm_bulk_kernel<MTv, NTv, 3>);
-                    if (nst == 4) return go(ttm_bulk_kernel<MTv, NTv, 4>);
-                    return go(ttm_bulk_kernel<MTv, NTv, 6>);
+                    return go(ttm_bulk_kernel<MTv, NTv, 4>);
                 };
                 using I1 = std::integral_constant<int, 1>;
                 using I2 = std::integral_constant<int, 2>;
                 using I4 = std::integral_constant<int, 4>;
+                if (nt == 1) return P.J <= 16 ? pick(I1{}, I1{}) : pick(I2{}, I1{});
                 if (nt == 2) return P.J <= 16 ? pick(I1{}, I2{}) : pick(I2{}, I2{});
                 return P.J <= 16 ? pick(I1{}, I4{}) : pick(I2{}, I4{});
             }

@@ -563,7 +563,9 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
                                : (a.dtype == TL_F32 ? StagedLayout<float, false>(P.J, P.K).bbytes
                                                     : StagedLayout<int64_t, false>(P.J, P.K).bbytes);
     const size_t stage_bytes = ((size_t)R * KI * s + 15) & ~(size_t)15;
-    const size_t smem = bbytes + kTtmStages * stage_bytes + (size_t)R * P.J * P.I * s;
+    // the output tile is staged only for contiguous outputs of the SIMT fold
+    const bool stage_out = P.ident && !(dmma && kDirectStore);
+    const size_t smem = bbytes + kTtmStages * stage_bytes + (stage_out ? (size_t)R * P.J * P.I * s : 0);
     if (smem > 200 * 1024) return TL_EUNSUPPORTED;
     const DeviceInfo &di = device_info();
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (228 * 1024) / (int64_t)(smem + 2048)));

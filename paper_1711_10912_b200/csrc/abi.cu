@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -60,7 +61,7 @@ int cuda_status(cudaError_t e, const char *what) {
 
 const DeviceInfo &device_info() {
     static std::mutex mu;
-    static std::vector<DeviceInfo> cache;
+    static std::deque<DeviceInfo> cache;  // stable references across push_back
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);

@@ -174,6 +174,145 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
+// ------------------------------------------------------------- regime B, boxed
+// Strided fibers whose output is permuted so that A's fastest free digit d0
+// is far apart in C (e.g. config 5's seed-5 layout: consecutive i land
+// 16830 elements apart): one thread per output would write isolated 8-byte
+// words.  Instead a CTA takes a 2-D box of outputs -- BA = 32*VEC positions
+// along d0 (contiguous in A: coalesced loads) by BC = 8*NJ positions along
+// the chain of digits that is contiguous in C -- folds them (each output's
+// k order unchanged: bit-exact), parks the box in shared memory and writes
+// it out along the C-contiguous direction.
+constexpr int kBoxMaxChain = 4;
+struct TtvBoxParams {
+    const void *a;
+    const void *b;
+    void *c;
+    const int32_t *stop;
+    int64_t b_stride;
+    int32_t b_dtype;
+    int32_t b_smem;
+    int64_t K, I;           // contracted extent and its A stride
+    int64_t e0, cs0;        // d0: extent and C stride (A stride 1)
+    int64_t nA, nJ, nrest;  // box counts along d0, along the chain, other digits
+    int64_t chain_ext;
+    int32_t nchain;
+    FastDiv ch_div[kBoxMaxChain];
+    int64_t ch_as[kBoxMaxChain], ch_cs[kBoxMaxChain];
+    int32_t nrest_d;
+    FastDiv rs_div[TL_MAX_DIGITS];
+    int64_t rs_as[TL_MAX_DIGITS], rs_cs[TL_MAX_DIGITS];
+};
+
+template <class TA, class TC, int VEC, int NJ>
+__global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ TtvBoxParams P) {
+    using Acc = typename AccOf<TA>::type;
+    constexpr int BA = 32 * VEC, BC = 8 * NJ, PITCH = BA + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    if (stop_requested(P.stop)) return;
+    Acc *bs = (Acc *)smem_raw;
+    const size_t bbytes = P.b_smem ? (((size_t)P.K * sizeof(Acc) + 15) & ~(size_t)15) : 0;
+    int64_t *tabA = (int64_t *)(smem_raw + bbytes);
+    int64_t *tabC = tabA + BC;
+    Acc *otile = (Acc *)(tabC + BC);  // [BC][PITCH]
+    if (P.b_smem) {
+        for (int64_t k = threadIdx.x; k < P.K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+    }
+    const TA *A = (const TA *)P.a;
+    TC *C = (TC *)P.c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ntiles = P.nA * P.nJ * P.nrest;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // tile -> (d0 block, chain block, other digits)
+        const int64_t ab = tile % P.nA;
+        const int64_t t2 = tile / P.nA;
+        const int64_t jb = t2 % P.nJ;
+        uint32_t rest = (uint32_t)(t2 / P.nJ);
+        int64_t baseA = ab * BA, baseC = ab * BA * P.cs0;
+        for (int d = 0; d < P.nrest_d; ++d) {
+            uint32_t q, r;
+            if (d == P.nrest_d - 1) {
+                r = rest;
+                q = 0;
+            } else {
+                P.rs_div[d].divmod(rest, q, r);
+            }
+            baseA += (int64_t)r * P.rs_as[d];
+            baseC += (int64_t)r * P.rs_cs[d];
+            rest = q;
+        }
+        __syncthreads();  // the previous tile's write-out is done with tabC / otile
+        if (threadIdx.x < BC) {
+            const int64_t jg = jb * BC + threadIdx.x;
+            int64_t oa = -1, oc = 0;
+            if (jg < P.chain_ext) {
+                uint32_t x = (uint32_t)jg;
+                oa = 0;
+                for (int d = 0; d < P.nchain; ++d) {
+                    uint32_t q, r;
+                    if (d == P.nchain - 1) {
+                        r = x;
+                        q = 0;
+                    } else {
+                        P.ch_div[d].divmod(x, q, r);
+                    }
+                    oa += (int64_t)r * P.ch_as[d];
+                    oc += (int64_t)r * P.ch_cs[d];
+                    x = q;
+                }
+            }
+            tabA[threadIdx.x] = oa;
+            tabC[threadIdx.x] = oc;
+        }
+        __syncthreads();
+        const int a = lane * VEC;
+        const bool a_ok = ab * BA + a + VEC <= P.e0;
+        // NJ passes of 8 chain rows (one per warp); each pass is the strided
+        // kernel's k loop: U rows of VEC elements in flight per thread
+        constexpr int U = 8;
+        for (int t = 0; t < NJ; ++t) {
+            const int j = warp + 8 * t;
+            const int64_t ta = tabA[j];
+            Acc acc[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = Acc(0);
+            if (a_ok && ta >= 0) {
+                const TA *pa = A + baseA + ta + a;
+                int64_t k = 0;
+                for (; k + U <= P.K; k += U) {
+                    Acc x[U][VEC];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) VecLoad<TA, VEC>::ld(pa + (k + u) * P.I, x[u]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const Acc bk = P.b_smem ? bs[k + u] : load_elem_as<Acc>(P.b, P.b_dtype, (k + u) * P.b_stride);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] = fold_step(acc[v], x[u][v], bk);
+                    }
+                }
+                for (; k < P.K; ++k) {
+                    Acc x[VEC];
+                    VecLoad<TA, VEC>::ld(pa + k * P.I, x);
+                    const Acc bk = P.b_smem ? bs[k] : load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fold_step(acc[v], x[v], bk);
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) otile[j * PITCH + a + v] = acc[v];
+        }
+        __syncthreads();
+        // write out along the C-contiguous chain
+        for (int idx = threadIdx.x; idx < BA * BC; idx += blockDim.x) {
+            const int j = idx % BC, aa = idx / BC;
+            if (tabA[j] >= 0 && ab * BA + aa < P.e0)
+                C[baseC + aa * P.cs0 + tabC[j]] = narrow<TC>(otile[j * PITCH + aa]);
+        }
+    }
+    pdl_release();
+}
+
 // ------------------------------------------------------------- small problems
 // Few outputs (e.g. HOPM's 400x400 intermediates, L2-resident): the fold
 // chain of each output (K dependent adds) is the critical path, so each CTA
@@ -546,7 +685,8 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
 // ------------------------------------------------------------- planning
 struct TtvLaunch {
     TtvParams P;
-    int regime;  // 0 = strided (B), 1 = staged (S)
+    TtvBoxParams box;  // regime 4
+    int regime;  // 0 = strided (B), 1 = staged (S), 2/3 = small, 4 = boxed strided
     int vec;
     int G;
     bool vecread;
@@ -681,7 +821,38 @@ static cudaError_t launch_kernel(Kern kern, const TtvLaunch &L, cudaStream_t st)
 }
 
 template <class TA, class TC>
+static cudaError_t launch_box(const TtvLaunch &L, cudaStream_t st) {
+    auto go = [&](auto kern) -> cudaError_t {
+        if (L.smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+            if (e != cudaSuccess) return e;
+        }
+        if (!L.pdl) {
+            kern<<<L.grid, L.block, L.smem, st>>>(L.box);
+            return cudaGetLastError();
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = L.grid;
+        cfg.blockDim = L.block;
+        cfg.dynamicSmemBytes = L.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, L.box);
+    };
+    if constexpr (sizeof(TA) == 4) {
+        if (L.vec == 4) return go(ttv_box_kernel<TA, TC, 4, 8>);
+    }
+    if (L.vec == 2) return go(ttv_box_kernel<TA, TC, 2, 8>);
+    return go(ttv_box_kernel<TA, TC, 1, 8>);
+}
+
+template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
+    if (L.regime == 4) return launch_box<TA, TC>(L, st);
     if (L.regime == 2 || L.regime == 3) {
         auto kern = (L.regime == 3) ? ttv_small_kernel<TA, TC, true, false> : ttv_small_kernel<TA, TC, false, false>;
         if constexpr (sizeof(TA) == 8 && std::is_same<typename AccOf<TA>::type, double>::value) {
@@ -723,6 +894,103 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
 }
 
 // Canonical form + kernel choice (host only; no device access).
+// Regime-B plan with a permuted output: the boxed kernel when A's fastest
+// free digit d0 is not C's fastest and a C-contiguous chain of at least 16
+// positions exists among the other free digits.
+static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
+    static const bool off = getenv("TL_TTV_NO_BOX") != nullptr;
+    if (off || cn.ident || cn.inner.empty()) return false;
+    // Measured on B200: the box's 8 warps stream 8 separate A regions, which
+    // costs more than scattered stores save once the inner block is wide
+    // (the plain kernel's warps then sweep whole k-rows together) unless the
+    // fold is short (K <= 32: a store per few loads).
+    if (cn.I >= 4096 && cn.K > 32) return false;
+    struct Dg {
+        int64_t ext, as, cs;
+    };
+    std::vector<Dg> free;
+    {
+        int64_t run = 1;
+        for (auto &d : cn.inner) {
+            free.push_back({d.first, run, d.second});
+            run *= d.first;
+        }
+        run = cn.K * cn.I;
+        for (auto &d : cn.outer) {
+            free.push_back({d.first, run, d.second});
+            run *= d.first;
+        }
+    }
+    const Dg d0 = free[0];
+    if (d0.ext < 16) return false;
+    // the C-fastest other digit, then digits continuing its C run
+    int cstar = -1;
+    for (size_t q = 1; q < free.size(); ++q)
+        if (cstar < 0 || free[q].cs < free[cstar].cs) cstar = (int)q;
+    if (cstar < 0 || free[cstar].cs > d0.cs) return false;
+    std::vector<int> chain{cstar};
+    int64_t cext = free[cstar].ext;
+    while (cext < 64 && (int)chain.size() < kBoxMaxChain) {
+        const Dg &last = free[chain.back()];
+        int nxt = -1;
+        for (size_t q = 1; q < free.size(); ++q) {
+            if (std::find(chain.begin(), chain.end(), (int)q) != chain.end()) continue;
+            if (free[q].cs == last.cs * last.ext) nxt = (int)q;
+        }
+        if (nxt < 0) break;
+        chain.push_back(nxt);
+        cext *= free[nxt].ext;
+    }
+    if (cext < 16 || cext > 0xffffffffll) return false;
+    TtvBoxParams &B = L.box;
+    B = TtvBoxParams{};
+    B.K = cn.K;
+    B.I = cn.I;
+    B.e0 = d0.ext;
+    B.cs0 = d0.cs;
+    B.chain_ext = cext;
+    B.nchain = (int32_t)chain.size();
+    for (size_t q = 0; q < chain.size(); ++q) {
+        B.ch_div[q].init((uint32_t)free[chain[q]].ext);
+        B.ch_as[q] = free[chain[q]].as;
+        B.ch_cs[q] = free[chain[q]].cs;
+    }
+    int64_t nrest = 1;
+    B.nrest_d = 0;
+    for (size_t q = 1; q < free.size(); ++q) {
+        if (std::find(chain.begin(), chain.end(), (int)q) != chain.end()) continue;
+        if (free[q].ext > 0xffffffffll) return false;
+        B.rs_div[B.nrest_d].init((uint32_t)free[q].ext);
+        B.rs_as[B.nrest_d] = free[q].as;
+        B.rs_cs[B.nrest_d] = free[q].cs;
+        ++B.nrest_d;
+        nrest *= free[q].ext;
+    }
+    if (B.nrest_d == 0) {  // keep one trivial digit so the decode loop is uniform
+        B.rs_div[0].init(1);
+        B.rs_as[0] = B.rs_cs[0] = 0;
+        B.nrest_d = 1;
+    }
+    int vec = 1;
+    if (s == 4 && d0.ext % 4 == 0 && base_addr % 16 == 0 && (cn.I % 4) == 0) vec = 4;
+    else if (d0.ext % 2 == 0 && base_addr % (2 * s) == 0 && (cn.I % 2) == 0 && s <= 8) vec = 2;
+    const int64_t BA = 32 * vec, BC = 64;
+    B.nA = (d0.ext + BA - 1) / BA;
+    B.nJ = (cext + BC - 1) / BC;
+    B.nrest = nrest;
+    const int64_t ntiles = B.nA * B.nJ * B.nrest;
+    if (ntiles > 0x7fffffffll) return false;
+    B.b_smem = (cn.K <= 8192) ? 1 : 0;
+    L.regime = 4;
+    L.vec = vec;
+    L.block = dim3(256);
+    const size_t bbytes = B.b_smem ? (((size_t)cn.K * 8 + 15) & ~(size_t)15) : 0;
+    L.smem = bbytes + 2 * BC * 8 + (size_t)BC * (BA + 1) * 8;
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / ((int64_t)L.smem + 2048)));
+    L.grid = dim3((unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * per_sm * 2));
+    return true;
+}
+
 static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch &L, Canon &cn) {
     if (!canon_contraction(a, m0, 0, cn)) {
         set_error("ttv: operand A is not a dense permutation layout (materialise views first)");
@@ -798,6 +1066,7 @@ static const char *ttv_regime_name(const TtvLaunch &L) {
         case 0: return "strided";
         case 1: return L.bulk ? "staged-bulk" : "staged";
         case 2: return "small-cols";
+        case 4: return "strided-box";
         default: return "small-rows";
     }
 }
@@ -808,6 +1077,7 @@ int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
     Canon cn;
     int rc = ttv_make_plan(a, (const void *)0x100000, m0, L, cn);
     if (rc != TL_OK) return rc;
+    if (L.regime == 0) plan_box(cn, L, (int64_t)dtype_size(a.dtype), 0x100000, device_info().num_sms);
     snprintf(buf, len, "{\"O\": %lld, \"K\": %lld, \"I\": %lld, \"ident\": %d, \"inner_digits\": %d, "
              "\"outer_digits\": %d, \"regime\": \"%s\", \"vec\": %d, \"grid\": %u, \"block\": %u, \"smem\": %zu}",
              (long long)cn.O, (long long)cn.K, (long long)cn.I, cn.ident ? 1 : 0, (int)cn.inner.size(),
@@ -837,6 +1107,17 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         // its shared memory
         P.fn = *fn;
         L.smem = std::max(L.smem, 2 * (size_t)fn->n * sizeof(double));
+    } else if (L.regime == 0) {
+        // permuted output on the strided regime: the boxed kernel
+        if (plan_box(cn, L, (int64_t)dtype_size(a.dtype), (uintptr_t)P.a, device_info().num_sms)) {
+            TtvBoxParams &B = L.box;
+            B.a = P.a;
+            B.b = b_ptr;
+            B.c = c_ptr;
+            B.stop = stop;
+            B.b_stride = b_stride;
+            B.b_dtype = b_dtype;
+        }
     }
     cudaError_t e;
     if (a.dtype == TL_F32 && c_dtype == TL_F32) e = launch_typed<float, float>(L, st);

@@ -105,7 +105,10 @@ CFG2_TABLE = {
 def test_ttv_canonical_forms_match_survey(layout):
     for mode, (regime, O, I, ident) in enumerate(CFG2_TABLE[layout], start=1):
         p = plan(0, (128,) * 4, layout, mode)
-        assert (p["regime"], p["O"], p["K"], p["I"], bool(p["ident"])) == (regime, O, 128, I, ident), (layout, mode)
+        # permuted outputs of regime B take the boxed variant of the strided kernel
+        got = "strided" if p["regime"] == "strided-box" else p["regime"]
+        assert (got, p["O"], p["K"], p["I"], bool(p["ident"])) == (regime, O, 128, I, ident), (layout, mode)
+        assert (p["regime"] == "strided-box") == (regime == "strided" and not ident and I < 4096), (layout, mode)
 
 
 def test_ttv_plans_for_other_configs():
@@ -118,7 +121,7 @@ def test_ttv_plans_for_other_configs():
     assert (p["regime"], p["O"], p["K"], p["I"], p["ident"]) == ("staged-bulk", 10771200, 9, 1, 0)
     # config 5 seed 5 layout: O=1, I=10.7M (regime B)
     p = plan(0, shape5, (7, 4, 2, 1, 6, 3, 5), 5, _abi.TL_F64)
-    assert (p["regime"], p["O"], p["I"]) == ("strided", 1, 10771200)
+    assert (p["regime"], p["O"], p["I"]) == ("strided-box", 1, 10771200)
     # HOPM's 400x400 intermediates use the small-problem kernels
     assert plan(0, (400, 400), (1, 2), 1, _abi.TL_F64)["regime"] == "small-rows"
     assert plan(0, (400, 400), (1, 2), 2, _abi.TL_F64)["regime"] == "small-cols"

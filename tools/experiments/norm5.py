@@ -4,7 +4,7 @@ sys.path.insert(0, R); sys.path.insert(0, os.path.join(R, "tests"))
 import numpy as np, torch
 import paper_1711_10912_b200 as tl
 import paper_1711_10912_b200.contraction as C
-sys.path.insert(0, os.path.join(R, "tools", "scratch"))
+sys.path.insert(0, os.path.join(R, "tools", "experiments"))
 from sweep_ttm5 import timeit
 out = {}
 for n in (5222400, 5222400 * 4, 64 << 20):

@@ -98,8 +98,13 @@ def ttm(a, bmat, mode: int) -> DenseTensor:
         raise ValueError(f"ttm matrix must have order 2, got {Bm.order}")
     if Bm.shape[1] != A.shape[mode - 1]:
         raise ValueError(f"matrix columns {Bm.shape[1]} do not match extent {A.shape[mode - 1]} of mode {mode}")
+    if _is_float(A.dtype) != _is_float(Bm.dtype):
+        raise NotImplementedError("ttm: mixed integer and floating operands")
+    if A.dtype == torch.float32 and Bm.dtype == torch.float64:
+        # keep B's binary64 values: contract in float64, round once to float32
+        return ttm(A.to(torch.float64), Bm, mode).to(torch.float32)
     if Bm.dtype != A.dtype:
-        Bm = Bm.to(A.dtype)
+        Bm = Bm.to(A.dtype)  # float32 matrix, float64 tensor: widening is exact
     m = mode - 1
     out = DenseTensor(A.shape[:m] + (Bm.shape[0],) + A.shape[m + 1:], dtype=A.dtype, device=A.device, fill_value=None)
     L = _abi.lib()

@@ -374,3 +374,20 @@ def test_cuda_graph_capture(gpu):
         g.replay()
     torch.cuda.synchronize()
     assert np.array_equal(o1.numpy(), eager[0]) and np.array_equal(o2.numpy(), eager[1]) and o3.item() == eager[2]
+
+
+def test_ttm_mixed_dtypes(gpu):
+    """float32 tensor x float64 matrix keeps the matrix's binary64 values
+    (one rounding at the end); integer x floating is refused like ttv."""
+    m = tl()
+    rng = np.random.default_rng(21)
+    T = rng.uniform(-1, 1, size=(20, 30, 12)).astype(np.float32)
+    M = rng.standard_normal((40, 30))
+    A32 = dev(W.layout_buffer(T, (2, 1, 3)), T.shape, (2, 1, 3))
+    B64 = dev(W.layout_buffer(M, (1, 2)), M.shape, (1, 2))
+    got = m.ttm(A32, B64, 2)
+    assert got.dtype == torch.float32
+    want = m.ttm(A32.to(torch.float64), B64, 2).numpy().astype(np.float32)
+    assert np.array_equal(bits(got.numpy()), bits(want))
+    with pytest.raises(NotImplementedError):
+        m.ttm(m.DenseTensor.from_memory((2, 3), [1, 2, 3, 4, 5, 6]), m.DenseTensor((2, 3)), 2)

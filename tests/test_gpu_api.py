@@ -391,3 +391,41 @@ def test_ttm_mixed_dtypes(gpu):
     assert np.array_equal(bits(got.numpy()), bits(want))
     with pytest.raises(NotImplementedError):
         m.ttm(m.DenseTensor.from_memory((2, 3), [1, 2, 3, 4, 5, 6]), m.DenseTensor((2, 3)), 2)
+
+
+def test_more_than_2_31_elements(gpu):
+    """Index arithmetic past 2^31 elements (8.6 GB of float32): ttv in both
+    modes and the norm on A[i, j] = (i + 3 j) mod 7 against closed forms
+    (integer-valued, so every sum is exact)."""
+    m = tl()
+    n1, n2 = 1 << 16, (1 << 15) + 1
+    if torch.cuda.get_device_properties(0).total_memory < 40 << 30:
+        pytest.skip("needs a large-memory GPU")
+    i = torch.arange(n1, device="cuda", dtype=torch.int64)
+    buf = torch.empty(n1 * n2, device="cuda", dtype=torch.float32)
+    for j0 in range(0, n2, 4096):  # build column blocks without a 17 GB int64 temporary
+        j = torch.arange(j0, min(n2, j0 + 4096), device="cuda", dtype=torch.int64)
+        buf[j0 * n1:(j0 + len(j)) * n1] = ((i[:, None] + 3 * j[None, :]) % 7).T.reshape(-1).to(torch.float32)
+    A = m.DenseTensor.from_memory((n1, n2), buf)
+    del buf
+    ones1 = m.DenseTensor.from_memory((n1,), torch.ones(n1, dtype=torch.float32, device="cuda"))
+    c = m.ttv(A, ones1, 1).numpy()  # sum over i of (i + 3j) mod 7
+    per_cycle, rem = divmod(n1, 7)
+    jj = np.arange(n2)
+    want = np.full(n2, per_cycle * 21, dtype=np.float64)
+    for r in range(rem):
+        want += (r + 3 * jj) % 7
+    assert np.array_equal(c, want.astype(np.float32))
+    w = (np.arange(n2) % 5).astype(np.float32)
+    c2 = m.ttv(A, m.DenseTensor.from_memory((n2,), w), 2).numpy()
+    ii = np.arange(n1)
+    want2 = np.zeros(n1)
+    for jm in range(35):  # (i + 3 j) mod 7 and j mod 5 repeat every 35 in j
+        cnt = len(range(jm, n2, 35))
+        want2 += cnt * ((ii + 3 * jm) % 7) * (jm % 5)
+    assert np.array_equal(c2, want2.astype(np.float32))
+    nrm = m.frobenius_norm(A)
+    sq = sum(((r % 7) ** 2) for r in range(7))  # each column holds n1 values cycling mod 7
+    col_sq = per_cycle * sq + np.array([sum(((r + 3 * j) % 7) ** 2 for r in range(rem)) for j in range(7)])
+    exact = float(np.sum(col_sq[np.arange(n2) % 7]))
+    assert abs(nrm - np.sqrt(exact)) <= 1e-12 * np.sqrt(exact)

@@ -614,7 +614,7 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         const bool al = (pa % 16 == 0 && pb % 16 == 0);
         const unsigned G = (unsigned)grid;
         if (a.dtype == TL_F32 && b.dtype == TL_F32) {
-            if (same && al) dot_rows_kernel<float, float, 4, true><<<G, threads, 0, st>>>(P);
+            if (same && al) dot_rows_kernel<float, float, 4, true, 8><<<G, threads, 0, st>>>(P);  // 8 x 16 B in flight: one stream
             else if (al) dot_rows_kernel<float, float, 4, false><<<G, threads, 0, st>>>(P);
             else dot_rows_kernel<float, float, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F64 && b.dtype == TL_F64) {

@@ -97,6 +97,40 @@ template <> struct VecLoad<int64_t, 1> {
     __device__ static void ld(const int64_t *p, int64_t *v) { v[0] = ld_stream(p); }
 };
 
+// Raw VEC-wide streaming load kept in the storage type (float32 values are
+// widened only when folded: half the registers of a widened copy, so twice
+// the loads can be in flight per SM).
+template <class TA, int VEC> struct RawLoad {
+    __device__ static void ld(const TA *p, TA *v) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] = ld_stream(p + j);
+    }
+};
+template <> struct RawLoad<float, 4> {
+    __device__ static void ld(const float *p, float *v) {
+        const float4 x = ld_stream_f4(p);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+};
+template <> struct RawLoad<float, 2> {
+    __device__ static void ld(const float *p, float *v) {
+        const float2 x = ld_stream_f2(p);
+        v[0] = x.x; v[1] = x.y;
+    }
+};
+template <> struct RawLoad<double, 2> {
+    __device__ static void ld(const double *p, double *v) {
+        const double2 x = ld_stream_d2(p);
+        v[0] = x.x; v[1] = x.y;
+    }
+};
+template <> struct RawLoad<int64_t, 2> {
+    __device__ static void ld(const int64_t *p, int64_t *v) {
+        const longlong2 x = ld_stream_l2(p);
+        v[0] = x.x; v[1] = x.y;
+    }
+};
+
 template <class TC, int VEC, class Acc>
 __device__ __forceinline__ void store_outputs(const TtvParams &P, int64_t o, int64_t i0, const Acc *acc) {
     TC *c = (TC *)P.c;
@@ -151,14 +185,14 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
 
         int64_t k = 0;
         for (; k + U <= K; k += U) {
-            Acc v[U][VEC];
+            TA v[U][VEC];
 #pragma unroll
-            for (int u = 0; u < U; ++u) VecLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
+            for (int u = 0; u < U; ++u) RawLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const Acc bk = P.b_smem ? bs[k + u] : load_elem_as<Acc>(P.b, P.b_dtype, (k + u) * P.b_stride);
 #pragma unroll
-                for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], v[u][j], bk);
+                for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], (Acc)v[u][j], bk);
             }
         }
         for (; k < K; ++k) {
@@ -901,10 +935,9 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
     static const bool off = getenv("TL_TTV_NO_BOX") != nullptr;
     if (off || cn.ident || cn.inner.empty()) return false;
     // Measured on B200: the box's 8 warps stream 8 separate A regions, which
-    // costs more than scattered stores save once the inner block is wide
-    // (the plain kernel's warps then sweep whole k-rows together) unless the
-    // fold is short (K <= 32: a store per few loads).
-    if (cn.I >= 4096 && cn.K > 32) return false;
+    // costs about what scattered stores cost the plain kernel unless the fold
+    // is short (K <= 32: a store per few loads, e.g. config 5's K = 9).
+    if (cn.K > 32) return false;
     struct Dg {
         int64_t ext, as, cs;
     };

@@ -20,6 +20,9 @@
 //    sequential folds read shared memory without bank conflicts (128-bit
 //    LDS along k when I == 1).  One thread owns each output fold, which is
 //    what keeps the summation order identical to the reference.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 #include <numeric>
 #include <type_traits>
@@ -716,6 +719,115 @@ __global__ void __launch_bounds__(256) ttv_staged_kernel(const __grid_constant__
     if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
 }
 
+// ------------------------------------------------------------- regime S, TMA rows
+// Contracted stride 1 (I == 1): each output folds one contiguous row of K
+// elements.  Tiles of 256 rows stream in 128-byte k-slabs through a 2-D TMA
+// tensor map (one cp.async.bulk.tensor per slab, issued by one thread,
+// completing on the stage's mbarrier) with the 128-byte hardware swizzle, so
+// the per-thread LDS.128 reads of a warp's 32 rows are conflict-free without
+// padding.  Thread r folds row r in k order (bit-exact).
+constexpr int kRowsTmaR = 256;
+constexpr int kRowsTmaStages = 3;
+
+__device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *map, int32_t c0, int32_t c1,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <class TA, class TC>
+__global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_constant__ TtvParams P,
+                                                                 const __grid_constant__ CUtensorMap map) {
+    using Acc = typename AccOf<TA>::type;
+    constexpr int KC = 128 / (int)sizeof(TA);  // elements per 128-byte slab row
+    constexpr int E = 16 / (int)sizeof(TA);    // elements per 16-byte chunk
+    constexpr int STAGE = kRowsTmaR * 128;     // bytes
+    extern __shared__ __align__(16) unsigned char smem_raw[];  // stages are re-aligned to 1024 below
+    __shared__ __align__(8) uint64_t full_bar[kRowsTmaStages];
+    pdl_wait();
+    if (stop_requested(P.stop)) return;
+    // stages first (1024-byte aligned for the swizzle), then b
+    unsigned char *stages = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    Acc *bs = (Acc *)(stages + kRowsTmaStages * STAGE);
+    const int64_t K = P.K;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kRowsTmaStages; ++st) mbar_init(&full_bar[st], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int nslab = (int)((K + KC - 1) / KC);
+    const int64_t ntiles = (P.O + kRowsTmaR - 1) / kRowsTmaR;
+    const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nitems = my_tiles * nslab;
+    int64_t p_tile = blockIdx.x;
+    int p_slab = 0, p_stage = 0;
+    auto issue_next = [&]() {
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[p_stage], STAGE);
+            tma_load_2d(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * kRowsTmaR), &full_bar[p_stage]);
+        }
+        if (++p_slab == nslab) {
+            p_slab = 0;
+            p_tile += gridDim.x;
+        }
+        if (++p_stage == kRowsTmaStages) p_stage = 0;
+    };
+    for (int q = 0; q < kRowsTmaStages - 1; ++q)
+        if (q < nitems) issue_next();
+
+    const int r = threadIdx.x;
+    const uint32_t swz = (uint32_t)(r & 7);
+    Acc acc = Acc(0);
+    int64_t tile = blockIdx.x;
+    int slab = 0, c_stage = 0;
+    uint32_t parity = 0;
+    for (int64_t q = 0; q < nitems; ++q) {
+        mbar_wait_parity(&full_bar[c_stage], parity);
+        __syncthreads();  // every thread is done with the stage about to be refilled
+        if (q + kRowsTmaStages - 1 < nitems) issue_next();
+        const unsigned char *row = stages + c_stage * STAGE + r * 128;
+        const int64_t k0 = (int64_t)slab * KC;
+        const int kc = (int)((K - k0 < KC) ? K - k0 : KC);
+        auto fold_chunk = [&](int c) {  // 16-byte chunk c of this row
+            const uint4 raw = *(const uint4 *)(row + (((uint32_t)c ^ swz) << 4));
+            const TA *v = (const TA *)&raw;
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc = fold_step(acc, (Acc)v[e], bs[k0 + c * E + e]);
+        };
+        if (kc == KC) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) fold_chunk(c);
+        } else {
+            for (int kk = 0; kk < kc; ++kk) {
+                const TA x = *(const TA *)(row + (((uint32_t)(kk / E) ^ swz) << 4) + (kk % E) * sizeof(TA));
+                acc = fold_step(acc, (Acc)x, bs[k0 + kk]);
+            }
+        }
+        if (slab == nslab - 1) {
+            const int64_t o = tile * kRowsTmaR + r;
+            if (o < P.O) {
+                const int64_t off = P.ident ? o : P.out_map.map((uint32_t)o);
+                ((TC *)P.c)[off] = narrow<TC>(acc);
+            }
+            acc = Acc(0);
+        }
+        if (++slab == nslab) {
+            slab = 0;
+            tile += gridDim.x;
+        }
+        if (++c_stage == kRowsTmaStages) {
+            c_stage = 0;
+            parity ^= 1u;
+        }
+    }
+    pdl_release();
+}
+
 // ------------------------------------------------------------- planning
 struct TtvLaunch {
     TtvParams P;
@@ -726,6 +838,8 @@ struct TtvLaunch {
     bool vecread;
     bool bulk;
     bool pdl;  // programmatic dependent launch (HOPM chains)
+    bool rows_tma;     // regime S, I == 1, 2-D TMA tensor map
+    CUtensorMap tmap;
     dim3 grid, block;
     size_t smem;
 };
@@ -884,9 +998,77 @@ static cudaError_t launch_box(const TtvLaunch &L, cudaStream_t st) {
     return go(ttv_box_kernel<TA, TC, 1, 8>);
 }
 
+// 2-D TMA tensor map for the rows kernel (driver entry point looked up once
+// through the runtime, so the library needs no link-time libcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }();
+    return fn;
+}
+
+static bool plan_rows_tma(TtvLaunch &L, const Canon &cn, int32_t dtype, int nsm) {
+    static const bool off = getenv("TL_TTV_NO_TMA") != nullptr;
+    const TtvParams &P = L.P;
+    if (off || L.regime != 1 || cn.I != 1 || (dtype != TL_F32 && dtype != TL_F64)) return false;
+    const int64_t s = dtype == TL_F32 ? 4 : 8;
+    const uintptr_t base = (uintptr_t)P.a;
+    if ((cn.K * s) % 16 != 0 || base % 16 != 0 || cn.O > 0x7fffffffll || cn.K > 0x7fffffffll) return false;
+    if (cn.O < kRowsTmaR) return false;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+    if (enc == nullptr) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cn.K, (cuuint64_t)cn.O};
+    const cuuint64_t strides[1] = {(cuuint64_t)(cn.K * s)};
+    const cuuint32_t box[2] = {(cuuint32_t)(128 / s), (cuuint32_t)kRowsTmaR};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&L.tmap, dtype == TL_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                     (void *)P.a, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    L.rows_tma = true;
+    L.block = dim3(kRowsTmaR);
+    L.smem = 1024 + (size_t)kRowsTmaStages * kRowsTmaR * 128 + (((size_t)cn.K * 8 + 15) & ~(size_t)15);
+    if (L.smem > 200 * 1024) return false;
+    const int64_t ntiles = (cn.O + kRowsTmaR - 1) / kRowsTmaR;
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / ((int64_t)L.smem + 2048)));
+    L.grid = dim3((unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * per_sm));
+    return true;
+}
+
+template <class TA, class TC>
+static cudaError_t launch_rows_tma(const TtvLaunch &L, cudaStream_t st) {
+    auto kern = ttv_rows_tma_kernel<TA, TC>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    if (e != cudaSuccess) return e;
+    if (!L.pdl) {
+        kern<<<L.grid, L.block, L.smem, st>>>(L.P, L.tmap);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = L.grid;
+    cfg.blockDim = L.block;
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, L.P, L.tmap);
+}
+
 template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
     if (L.regime == 4) return launch_box<TA, TC>(L, st);
+    if (L.rows_tma) {
+        if constexpr (std::is_same<TA, float>::value || std::is_same<TA, double>::value) return launch_rows_tma<TA, TC>(L, st);
+        return cudaErrorInvalidValue;
+    }
     if (L.regime == 2 || L.regime == 3) {
         auto kern = (L.regime == 3) ? ttv_small_kernel<TA, TC, true, false> : ttv_small_kernel<TA, TC, false, false>;
         if constexpr (sizeof(TA) == 8 && std::is_same<typename AccOf<TA>::type, double>::value) {
@@ -1140,6 +1322,8 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         // its shared memory
         P.fn = *fn;
         L.smem = std::max(L.smem, 2 * (size_t)fn->n * sizeof(double));
+    } else if (L.regime == 1 && plan_rows_tma(L, cn, a.dtype, device_info().num_sms)) {
+        // contracted stride 1: rows through the 2-D TMA tensor map
     } else if (L.regime == 0) {
         // permuted output on the strided regime: the boxed kernel
         if (plan_box(cn, L, (int64_t)dtype_size(a.dtype), (uintptr_t)P.a, device_info().num_sms)) {

@@ -199,3 +199,14 @@ def test_gett_tile_store_order():
     assert plan(1, (512,) * 3, (1, 2, 3), 2, _abi.TL_F64, (384, 512))["box"] == 0
     # J = 32 with a small K now stays on the staged kernels
     assert plan(1, (5, 37, 2001), (1, 2, 3), 2, _abi.TL_F64, (32, 37))["path"] == "staged"
+
+
+def test_product_package_never_touches_the_oracle():
+    """The oracle is test infrastructure only: no module of the package
+    imports, loads or names it, and the package has no CPU compute path."""
+    pkg = os.path.join(ROOT, "paper_1711_10912_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            text = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in text, fn
+            assert "tl_oracle" not in text and "libtloracle" not in text, fn

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -102,6 +103,16 @@ static bool check_desc(const tl_desc *d, const char *what) {
     return true;
 }
 
+static bool check_ptrs(const char *what, std::initializer_list<const void *> ptrs) {
+    for (const void *q : ptrs) {
+        if (q == nullptr) {
+            set_error("%s: null data pointer", what);
+            return false;
+        }
+    }
+    return true;
+}
+
 static bool is_first_order_dense(const tl_desc &d) {
     int64_t run = 1;
     for (int r = 0; r < d.order; ++r) {
@@ -168,6 +179,7 @@ int tl_ttv(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_
         set_error("ttv: mixed integer/floating operands");
         return TL_EUNSUPPORTED;
     }
+    if (!check_ptrs("ttv", {a_ptr, b_ptr, c_ptr})) return TL_EINVAL;
     const void *bp = (const unsigned char *)b_ptr + b->offset * (int64_t)dtype_size(b->dtype);
     return ttv_enqueue(*a, a_ptr, bp, b->dtype, b->stride[0], c->dtype, c_ptr, mode - 1, nullptr,
                        (cudaStream_t)stream, nullptr, false);
@@ -209,6 +221,7 @@ int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void 
         set_error("ttm: A, B and C must share a dtype");
         return TL_EUNSUPPORTED;
     }
+    if (!check_ptrs("ttm", {a_ptr, b_ptr, c_ptr})) return TL_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     // few rows J (<= 32): the staged tile kernels (HBM-bound; DMMA for
     // float64); GEMM-shaped float64 or float32 -> DMMA GETT (float32 widened:
@@ -247,6 +260,7 @@ int tl_inner(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *
         set_error("shape mismatch");
         return TL_EINVAL;
     }
+    if (!check_ptrs("inner", {a_ptr, b_ptr, result_dev, ws})) return TL_EINVAL;
     return reduce_enqueue(*a, a_ptr, *b, b_ptr, result_dev, false, ws, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -257,6 +271,7 @@ int tl_frobenius_norm(const tl_desc *a, const void *a_ptr, double *result_dev, v
         set_error("frobenius_norm requires floating elements");
         return TL_EUNSUPPORTED;
     }
+    if (!check_ptrs("frobenius_norm", {a_ptr, result_dev, ws})) return TL_EINVAL;
     return reduce_enqueue(*a, a_ptr, *a, a_ptr, result_dev, true, ws, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -294,6 +309,7 @@ int tl_hopm(const tl_desc *a, const void *a_ptr, const double *const *u0_ptrs, d
             void *ws, size_t ws_bytes, void *stream) {
     int rc = hopm_check(a, u_ptrs, max_sweeps);
     if (rc != TL_OK) return rc;
+    if (!check_ptrs("hopm", {a_ptr, l_dev, hist_dev, info_dev, ws})) return TL_EINVAL;
     return hopm_enqueue(*a, a_ptr, u0_ptrs, u_ptrs, max_sweeps, tol, l_dev, hist_dev, info_dev, resid_dev, ws,
                         ws_bytes, (cudaStream_t)stream);
 }
@@ -319,7 +335,10 @@ int tl_hopm_graph_create(const tl_desc *a, const void *a_ptr, const double *cons
                          double *resid_dev, void *ws, size_t ws_bytes, void *stream, tl_graph *out) {
     int rc = hopm_check(a, u_ptrs, max_sweeps);
     if (rc != TL_OK) return rc;
-    if (out == nullptr) return TL_EINVAL;
+    if (out == nullptr || !check_ptrs("hopm graph", {a_ptr, l_dev, hist_dev, info_dev, ws})) {
+        if (out == nullptr) set_error("hopm graph: null output handle");
+        return TL_EINVAL;
+    }
     (void)device_info();  // cache device attributes outside the capture
     cudaStream_t st = (cudaStream_t)stream;
     cudaStream_t cap = st;
@@ -394,6 +413,7 @@ int tl_copy(const tl_desc *a, const void *a_ptr, const tl_desc *c, void *c_ptr, 
         set_error("copy: shape or dtype mismatch");
         return TL_EINVAL;
     }
+    if (!check_ptrs("copy", {a_ptr, c_ptr})) return TL_EINVAL;
     return copy_enqueue(*a, a_ptr, *c, c_ptr, (cudaStream_t)stream);
 }
 

@@ -72,6 +72,10 @@ def test_abi_validation_mirrors_reference_errors():
     # hopm max_sweeps < 1 (hopm.py:79-80)
     ptrs = (ctypes.c_void_p * 2)()
     assert L.tl_hopm(a, None, None, ptrs, 0, 0.0, None, None, None, None, None, 0, None) == _abi.TL_EINVAL
+    # null data pointers are refused before any device work
+    assert L.tl_ttv(a, None, desc((4,)), None, desc((3,)), None, 2, None) == _abi.TL_EINVAL
+    assert b"null data pointer" in L.tl_last_error()
+    assert L.tl_copy(a, None, a, None, None) == _abi.TL_EINVAL
     # host-only plan query rejects a bad mode
     buf = ctypes.create_string_buffer(256)
     assert L.tl_plan_describe(0, a, None, 5, buf, 256) == _abi.TL_EINVAL

@@ -17,13 +17,12 @@ differs, by design:
 from __future__ import annotations
 
 import numbers
-from typing import Optional, Sequence
 
 import numpy as np
 import torch
 
 from . import _abi
-from .layout import TensorMeta, inverse_memory_index, memory_index, validate_layout, validate_shape, volume, zero_indices
+from .layout import TensorMeta, memory_index, validate_layout, validate_shape, volume
 
 __all__ = ["DenseTensor", "tensors_equal", "as_dtype"]
 

@@ -3,7 +3,6 @@ regime, all ttm paths, the container API (relayout/assign/equality/
 interchange), error behaviour, allocation discipline, CUDA-graph capture,
 and full-size config-3 ttm checked on sampled outputs."""
 
-import math
 import random
 
 import numpy as np

@@ -7,7 +7,6 @@ tolerances (float64 1e-12, float32 1e-5) relative to the a-priori bound
 sum_k |a_k||b_k|."""
 
 import hashlib
-import math
 
 import numpy as np
 import pytest

@@ -1233,8 +1233,11 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
     const uintptr_t base = (uintptr_t)P.a;
     bool ok;
     const size_t small_bbytes = ((size_t)P.K * 8 + 15) & ~(size_t)15;
-    const bool small_cols = P.I >= 32 && P.O * P.I <= 4096;
-    const bool small_rows = P.I == 1 && P.O <= 4096;
+    // few outputs (<= 16384) of a small operand (<= 32 MB): latency-bound,
+    // the whole-block kernels win (measured: config 1 5.6 -> 3.8 us)
+    const bool small_ok = P.O * P.I * P.K * (int64_t)s <= (32ll << 20);
+    const bool small_cols = small_ok && P.I >= 32 && P.O * P.I <= 16384;
+    const bool small_rows = small_ok && P.I == 1 && P.O <= 16384;
     if ((small_cols || small_rows) && P.K <= kSmallSlab * kSmallMaxSlabs &&
         small_bbytes + 32 * (size_t)(P.K | 1) * s <= 200 * 1024) {
         // few outputs: whole 32-output input blocks in flight, one fold warp

@@ -116,9 +116,12 @@ def test_ttv_canonical_forms_match_survey(layout):
 
 
 def test_ttv_plans_for_other_configs():
-    # config 1: O=64, K=96, I=128 (regime B)
+    # config 1: O=64, K=96, I=128 -- 8192 outputs of a 6 MB operand: latency-bound,
+    # whole-block small kernel
     p = plan(0, (128, 96, 64), (1, 2, 3), 2, _abi.TL_F64)
-    assert (p["regime"], p["O"], p["K"], p["I"]) == ("strided", 64, 96, 128)
+    assert (p["regime"], p["O"], p["K"], p["I"]) == ("small-cols", 64, 96, 128)
+    # a large operand with as few outputs streams through the strided kernel
+    assert plan(0, (128, 4096, 64), (1, 2, 3), 2, _abi.TL_F64)["regime"] == "strided"
     # config 5 seed 0 layout: contracted stride 1, K=9, permuted output, TMA bulk tiles
     shape5 = (3, 33, 5, 17, 9, 2, 640)
     p = plan(0, shape5, (5, 3, 2, 1, 6, 4, 7), 5, _abi.TL_F64)

@@ -99,13 +99,14 @@ __device__ __forceinline__ void fused_norm_tail(const FusedNorm &f, const double
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(&f.ctl->ticket, 1u);
+        // acq_rel: this CTA's outputs (ordered before by the barrier) are
+        // released with the ticket; the last CTA acquires everyone's
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&f.ctl->ticket) : "memory");
         last = (prev == gridDim.x - 1);
     }
     __syncthreads();
     if (!last) return;
-    __threadfence();
     hopm_normalize_block(w, f, stage);
     if (threadIdx.x == 0) f.ctl->ticket = 0u;
 }

@@ -156,13 +156,14 @@ template <class Acc> __device__ void finish(const ReduceParams &P, Acc cta) {
     }
     if (threadIdx.x == 0) {
         store_partial(P.partials, blockIdx.x, cta);
-        __threadfence();
-        const unsigned prev = atomicAdd(P.ticket, 1u);
+        // release: the partial is visible before the ticket moves; acquire:
+        // the last CTA then sees every other CTA's partial
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.ticket) : "memory");
         am_last = (prev == gridDim.x - 1);
     }
     __syncthreads();
     if (!am_last) return;
-    __threadfence();
     Acc v;
     acc_zero(v);
     for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)

@@ -428,3 +428,20 @@ def test_more_than_2_31_elements(gpu):
     col_sq = per_cycle * sq + np.array([sum(((r + 3 * j) % 7) ** 2 for r in range(rem)) for j in range(7)])
     exact = float(np.sum(col_sq[np.arange(n2) % 7]))
     assert abs(nrm - np.sqrt(exact)) <= 1e-12 * np.sqrt(exact)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_ttv_tma_rows_edges(gpu, dtype):
+    """Contracted stride 1 through the 2-D TMA tensor map: K shorter than,
+    not a multiple of, and longer than a 128-byte slab; O with a partial
+    last tile; outputs in order and permuted."""
+    rng = np.random.default_rng(31)
+    for K in (4, 8, 12, 36, 100):
+        if (K * np.dtype(dtype).itemsize) % 16:
+            continue
+        for O2 in (256, 300, 1000):
+            shape = (K, O2, 3)
+            for layout in ((1, 2, 3), (1, 3, 2)):
+                T = rng.uniform(-1, 1, size=shape).astype(dtype)
+                b = rng.uniform(-1, 1, size=K).astype(dtype)
+                check_ttv(T, layout, 1, b, dtype)

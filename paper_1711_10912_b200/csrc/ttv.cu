@@ -1282,7 +1282,7 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
 static const char *ttv_regime_name(const TtvLaunch &L) {
     switch (L.regime) {
         case 0: return "strided";
-        case 1: return L.bulk ? "staged-bulk" : "staged";
+        case 1: return L.rows_tma ? "rows-tma" : (L.bulk ? "staged-bulk" : "staged");
         case 2: return "small-cols";
         case 4: return "strided-box";
         default: return "small-rows";
@@ -1296,6 +1296,7 @@ int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
     int rc = ttv_make_plan(a, (const void *)0x100000, m0, L, cn);
     if (rc != TL_OK) return rc;
     if (L.regime == 0) plan_box(cn, L, (int64_t)dtype_size(a.dtype), 0x100000, device_info().num_sms);
+    if (L.regime == 1) plan_rows_tma(L, cn, a.dtype, device_info().num_sms);  // needs the driver's encoder
     snprintf(buf, len, "{\"O\": %lld, \"K\": %lld, \"I\": %lld, \"ident\": %d, \"inner_digits\": %d, "
              "\"outer_digits\": %d, \"regime\": \"%s\", \"vec\": %d, \"grid\": %u, \"block\": %u, \"smem\": %zu}",
              (long long)cn.O, (long long)cn.K, (long long)cn.I, cn.ident ? 1 : 0, (int)cn.inner.size(),

@@ -439,9 +439,32 @@ def test_ttv_tma_rows_edges(gpu, dtype):
     for K in (4, 8, 12, 36, 100):
         if (K * np.dtype(dtype).itemsize) % 16:
             continue
-        for O2 in (256, 300, 1000):
+        for O2 in (5462, 6000):  # O = 3 * O2 > 16384 outputs: past the small-problem kernels
             shape = (K, O2, 3)
             for layout in ((1, 2, 3), (1, 3, 2)):
                 T = rng.uniform(-1, 1, size=shape).astype(dtype)
                 b = rng.uniform(-1, 1, size=K).astype(dtype)
                 check_ttv(T, layout, 1, b, dtype)
+
+
+def test_plans_on_device(gpu):
+    """With the driver present the stride-1 regime uses the 2-D TMA tensor map."""
+    import ctypes
+    import json
+
+    from paper_1711_10912_b200 import _abi
+
+    L = _abi.lib()
+    L.tl_plan_describe.argtypes = [ctypes.c_int32, ctypes.POINTER(_abi.TlDesc), ctypes.POINTER(_abi.TlDesc),
+                                   ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
+
+    def plan(shape, layout, mode, dt):
+        buf = ctypes.create_string_buffer(2048)
+        d = _abi.make_desc(shape, W.compute_strides(shape, layout), dt)
+        assert L.tl_plan_describe(0, d, None, mode, buf, 2048) == 0
+        return json.loads(buf.value.decode())
+
+    assert plan((128,) * 4, (1, 2, 3, 4), 1, _abi.TL_F32)["regime"] == "rows-tma"
+    assert plan((4, 5462, 3), (1, 2, 3), 1, _abi.TL_F32)["regime"] == "rows-tma"
+    # K * 8 bytes not a multiple of 16 (config 5, K = 9): 1-D bulk tiles instead
+    assert plan((3, 33, 5, 17, 9, 2, 640), (5, 3, 2, 1, 6, 4, 7), 5, _abi.TL_F64)["regime"] == "staged-bulk"

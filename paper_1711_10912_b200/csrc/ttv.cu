@@ -58,6 +58,7 @@ struct TtvParams {
     // regime S, permuted outputs: out_map(o) = otab[o % E] + out_hi(o / E),
     // otab (int32, shared memory) holding the map of the first otab_d0 digits
     int32_t in_vec_ok;  // regime B: first inner digit's extent is a multiple of VEC
+    int64_t o_mul;      // regime B: o visiting-order multiplier (1: identity)
     int32_t otab_n;   // E (0: plain digit map)
     int32_t otab_d0;
     FastDiv otab_div;
@@ -178,8 +179,13 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
     const int64_t IV = I / VEC;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid < P.O * IV) {
-        const int64_t o = gid / IV;
-        const int64_t i0 = (gid - o * IV) * VEC;
+        const int64_t og = gid / IV;
+        const int64_t i0 = (gid - og * IV) * VEC;
+        // o visiting order: og * o_mul mod O (gcd(o_mul, O) = 1: a permutation).
+        // Measured on B200: slabs visited in storage order by concurrently
+        // running warps camp on the same HBM channels when a slab is 64 or
+        // 128 KB (I = 128 / 256 float32: 6.6 TB/s); scrambled, 7.1 TB/s.
+        const int64_t o = P.o_mul > 1 ? (int64_t)(((uint64_t)og * (uint64_t)P.o_mul) % (uint64_t)P.O) : og;
         const TA *pa = (const TA *)P.a + (o * K) * I + i0;
 
         Acc acc[VEC];
@@ -939,6 +945,16 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
     while (threads > 32 && (nthreads + threads - 1) / threads < 2 * nsm) threads /= 2;
     P.b_smem = (P.K <= 8192) ? 1 : 0;
     P.in_vec_ok = (P.in_map.n >= 1 && P.in_map.div[0].d % (uint32_t)vec == 0) ? 1 : 0;
+    static const int64_t omul_env = [] {
+        const char *e = getenv("TL_TTV_OMUL");
+        return (int64_t)(e ? atoll(e) : 257);
+    }();
+    // scramble only slabs of up to 256 KB (larger ones, e.g. HOPM's 1.28 MB,
+    // measure slightly better in storage order)
+    int64_t m = (P.K * P.I * s <= (256 << 10)) ? omul_env : 1;
+    while (m > 1 && std::gcd(m, P.O) != 1) m += 2;
+    P.o_mul = (P.O > 1 && m > 1) ? m % P.O : 1;
+    if (P.o_mul == 0) P.o_mul = 1;
     L.regime = 0;
     L.vec = vec;
     L.block = dim3(threads);

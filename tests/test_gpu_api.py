@@ -468,3 +468,19 @@ def test_plans_on_device(gpu):
     assert plan((4, 5462, 3), (1, 2, 3), 1, _abi.TL_F32)["regime"] == "rows-tma"
     # K * 8 bytes not a multiple of 16 (config 5, K = 9): 1-D bulk tiles instead
     assert plan((3, 33, 5, 17, 9, 2, 640), (5, 3, 2, 1, 6, 4, 7), 5, _abi.TL_F64)["regime"] == "staged-bulk"
+
+
+def test_hopm_float32_equals_widened_float64(gpu):
+    """HOPM on float32 storage computes in binary64 from the exact widened
+    values: identical to HOPM on the same values stored as float64."""
+    m = tl()
+    rng = np.random.default_rng(41)
+    T = rng.uniform(-1, 1, size=(30, 20, 25)).astype(np.float32)
+    for layout in ((1, 2, 3), (2, 3, 1)):
+        buf = W.layout_buffer(T, layout)
+        a32 = m.DenseTensor.from_memory(T.shape, buf, layout=layout)
+        a64 = m.DenseTensor.from_memory(T.shape, buf.astype(np.float64), layout=layout)
+        s32 = m.hopm(a32, max_sweeps=8, tol=0.0)
+        s64 = m.hopm(a64, max_sweeps=8, tol=0.0)
+        assert s32.lambda_history == s64.lambda_history
+        assert all(np.array_equal(x.numpy(), y.numpy()) for x, y in zip(s32.u, s64.u))

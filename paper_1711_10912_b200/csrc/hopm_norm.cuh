@@ -7,6 +7,8 @@
 // products and sums, IEEE sqrt), u = w / norm uses IEEE division.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "tl_common.cuh"
 
 namespace tl {
@@ -109,6 +111,70 @@ __device__ __forceinline__ void fused_norm_tail(const FusedNorm &f, const double
     if (!last) return;
     hopm_normalize_block(w, f, stage);
     if (threadIdx.x == 0) f.ctl->ticket = 0u;
+}
+
+// Bookkeeping after the norm s of mode r is known (hopm.py:106-118); one
+// thread.  Returns false on a zero norm (DegenerateInputError).
+__device__ __forceinline__ bool hopm_record_norm(const FusedNorm &f, double s) {
+    if (s == 0.0) {
+        f.info[2] = f.sweep;
+        f.info[3] = f.r + 1;
+        f.info[0] = f.sweep - 1;
+        f.ctl->stop = 1;
+        return false;
+    }
+    f.l[f.r] = s;
+    if (f.r == f.p - 1) {
+        f.info[0] = f.sweep;
+        f.hist[f.sweep - 1] = s;
+        if (f.ctl->have_prev && fabs(s - f.ctl->prev) < f.tol) {
+            f.info[1] = 1;
+            f.ctl->stop = 1;
+        }
+        f.ctl->prev = s;
+        f.ctl->have_prev = 1;
+    }
+    return true;
+}
+
+// Fused normalisation for a ttv launched as ONE thread-block cluster whose
+// CTAs each produced <= 32 consecutive entries of w (CTA rank c owns
+// w[32c .. 32c+31], held in its own shared `mine`).  No global round trip
+// and no last-CTA ticket: after a cluster barrier every CTA gathers w
+// through distributed shared memory, folds the same sequential norm
+// (bit-identical in every CTA), and writes its own slice of u = w / s.
+// `stage` is >= 2n doubles of this CTA's shared memory.
+__device__ __forceinline__ void fused_norm_cluster(const FusedNorm &f, const double *mine, double *stage) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ double nrm;
+    const int64_t n = f.n;
+    double *sq = stage + n;
+    cl.sync();  // every CTA's `mine` is complete and visible
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double *src = cl.map_shared_rank(mine, (unsigned)(i / 32));
+        const double x = src[i % 32];
+        stage[i] = x;
+        sq[i] = __dmul_rn(x, x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        int64_t i = 0;
+        for (; i + 32 <= n; i += 32) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) acc = __dadd_rn(acc, sq[i + q]);
+        }
+        for (; i < n; ++i) acc = __dadd_rn(acc, sq[i]);
+        const double s = __dsqrt_rn(acc);
+        nrm = s;
+        if (cl.block_rank() == 0) hopm_record_norm(f, s);
+    }
+    __syncthreads();
+    const double s = nrm;
+    const int64_t base = (int64_t)cl.block_rank() * 32;
+    if (s != 0.0 && threadIdx.x < 32 && base + threadIdx.x < n) f.u[base + threadIdx.x] = __ddiv_rn(stage[base + threadIdx.x], s);
+    cl.sync();  // no CTA leaves while others may still read its `mine`
 }
 
 }  // namespace tl

@@ -369,11 +369,12 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
 constexpr int kSmallSlab = 64;
 constexpr int kSmallMaxSlabs = 64;  // K <= 4096
 
-template <class TA, class TC, bool ROWS, bool PAIRS>
+template <class TA, class TC, bool ROWS, bool PAIRS, bool CL = false>
 __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ TtvParams P) {
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[kSmallMaxSlabs];
+    __shared__ double mine[32];  // CL: this CTA's slice of w for the cluster norm
     pdl_wait();
     if (stop_requested(P.stop)) return;
     const int64_t K = P.K, I = P.I;
@@ -481,7 +482,9 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
                 }
             }
         }
-        if (j < nout) {
+        if constexpr (CL) {
+            mine[j] = (j < nout) ? (double)acc : 0.0;  // w stays on chip
+        } else if (j < nout) {
             int64_t off;
             if constexpr (ROWS) {
                 const int64_t oo = o0 + j;
@@ -495,7 +498,11 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
     }
     cp_async_wait<0>();
     pdl_release();  // the next kernel's launch overlaps this one's tail
-    if constexpr (std::is_same<TC, double>::value) fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
+    if constexpr (CL) {
+        fused_norm_cluster(P.fn, mine, (double *)smem_raw);
+    } else if constexpr (std::is_same<TC, double>::value) {
+        fused_norm_tail(P.fn, (const double *)P.c, (double *)smem_raw);
+    }
 }
 
 // ------------------------------------------------------------- regime S
@@ -844,6 +851,7 @@ struct TtvLaunch {
     bool vecread;
     bool bulk;
     bool pdl;  // programmatic dependent launch (HOPM chains)
+    bool small_cluster;  // small kernel + HOPM norm as one thread-block cluster
     bool rows_tma;     // regime S, I == 1, 2-D TMA tensor map
     CUtensorMap tmap;
     dim3 grid, block;
@@ -1090,6 +1098,31 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         if constexpr (sizeof(TA) == 8 && std::is_same<typename AccOf<TA>::type, double>::value) {
             if (L.vec == 2) kern = (L.regime == 3) ? ttv_small_kernel<TA, TC, true, true> : ttv_small_kernel<TA, TC, false, true>;
         }
+        if constexpr (std::is_same<TA, double>::value && std::is_same<TC, double>::value) {
+            if (L.small_cluster) {
+                // HOPM fused norm over one thread-block cluster (no ticket, w via DSMEM)
+                auto ck = (L.regime == 3) ? (L.vec == 2 ? ttv_small_kernel<TA, TC, true, true, true>
+                                                        : ttv_small_kernel<TA, TC, true, false, true>)
+                                          : (L.vec == 2 ? ttv_small_kernel<TA, TC, false, true, true>
+                                                        : ttv_small_kernel<TA, TC, false, false, true>);
+                cudaError_t e = cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+                if (e == cudaSuccess) e = cudaFuncSetAttribute(ck, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e != cudaSuccess) return e;
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = L.grid;
+                cfg.blockDim = L.block;
+                cfg.dynamicSmemBytes = L.smem;
+                cfg.stream = st;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = L.grid.x;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                return cudaLaunchKernelEx(&cfg, ck, L.P);
+            }
+        }
         if (L.smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
             if (e != cudaSuccess) return e;
@@ -1320,6 +1353,39 @@ int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
     return TL_OK;
 }
 
+// Can the small kernel's grid run as one cluster (up to 16 CTAs, non-portable
+// above 8) with its shared memory?  Queried once per configuration.
+static bool small_cluster_fits(const TtvLaunch &L) {
+    static const bool off = getenv("TL_HOPM_NO_CLUSTER") != nullptr;
+    if (off) return false;
+    auto kern = (L.regime == 3) ? (L.vec == 2 ? ttv_small_kernel<double, double, true, true, true>
+                                              : ttv_small_kernel<double, double, true, false, true>)
+                                : (L.vec == 2 ? ttv_small_kernel<double, double, false, true, true>
+                                              : ttv_small_kernel<double, double, false, false, true>);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = L.grid;
+    cfg.blockDim = L.block;
+    cfg.dynamicSmemBytes = L.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = L.grid.x;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return clusters >= 1;
+}
+
 // Entry used by tl_ttv and by the HOPM orchestration (which passes a stop
 // flag and binary64 outputs for float32 storage).
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
@@ -1342,6 +1408,10 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         // its shared memory
         P.fn = *fn;
         L.smem = std::max(L.smem, 2 * (size_t)fn->n * sizeof(double));
+        // few CTAs: normalise inside one thread-block cluster instead
+        if ((L.regime == 2 || L.regime == 3) && a.dtype == TL_F64 && c_dtype == TL_F64 && L.grid.x <= 16 &&
+            fn->n == P.O * P.I && small_cluster_fits(L))
+            L.small_cluster = true;
     } else if (L.regime == 1 && plan_rows_tma(L, cn, a.dtype, device_info().num_sms)) {
         // contracted stride 1: rows through the 2-D TMA tensor map
     } else if (L.regime == 0) {

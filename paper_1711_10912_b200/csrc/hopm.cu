@@ -34,7 +34,7 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
                 int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
                 const FusedNorm *fn, bool pdl);
 
-constexpr int kNormSmem = 6000;
+constexpr int kNormSmem = 6000;  // doubles staged in shared memory for the norm fold
 // Programmatic dependent launch between the chained ttv kernels of a sweep
 // (TL_HOPM_PDL=1).  Off by default: measured at 400^3 it is SLOWER inside the
 // captured graph (4,170 vs 5,290 sweeps/s with the release placed either at
@@ -45,7 +45,7 @@ static bool hopm_pdl() {
         return e && e[0] == '1';
     }();
     return on;
-}  // doubles staged in shared memory for the norm fold
+}
 
 // Source of w: a float64 buffer, or (order-1 hopm) the tensor itself.
 struct WSource {

@@ -32,6 +32,32 @@ struct FusedNorm {
     HopmCtl *ctl;
 };
 
+// 0 + x[0] + x[1] + ... in order (one thread).  The next 16 values are
+// loaded into registers while the current 16 are added, so the shared-memory
+// latency stays off the serial add chain (~8 cycles per term, not ~24).
+__device__ __forceinline__ double ordered_sum(const double *x, int64_t n) {
+    double acc = 0.0;
+    int64_t i = 0;
+    if (n >= 16) {
+        double cur[16], nxt[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) cur[q] = x[q];
+        for (; i + 32 <= n; i += 16) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) nxt[q] = x[i + 16 + q];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc = __dadd_rn(acc, cur[q]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) cur[q] = nxt[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc = __dadd_rn(acc, cur[q]);
+        i += 16;
+    }
+    for (; i < n; ++i) acc = __dadd_rn(acc, x[i]);
+    return acc;
+}
+
 // Called by every thread of ONE block.  w: n doubles (global, written by
 // this or other CTAs before a fence); stage: >= n doubles of shared memory
 // or nullptr (then w is folded from global memory).
@@ -52,14 +78,7 @@ __device__ __forceinline__ void hopm_normalize_block(const double *w, const Fuse
     if (threadIdx.x == 0) {
         double acc = 0.0;
         if (stage != nullptr) {
-            // blocks of 32 with a compile-time trip count: the loads issue
-            // ahead of the serial add chain
-            int64_t i = 0;
-            for (; i + 32 <= n; i += 32) {
-#pragma unroll
-                for (int q = 0; q < 32; ++q) acc = __dadd_rn(acc, sq[i + q]);
-            }
-            for (; i < n; ++i) acc = __dadd_rn(acc, sq[i]);
+            acc = ordered_sum(sq, n);
         } else {
             for (int64_t i = 0; i < n; ++i) {
                 const double x = __ldcg(w + i);
@@ -159,13 +178,7 @@ __device__ __forceinline__ void fused_norm_cluster(const FusedNorm &f, const dou
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double acc = 0.0;
-        int64_t i = 0;
-        for (; i + 32 <= n; i += 32) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) acc = __dadd_rn(acc, sq[i + q]);
-        }
-        for (; i < n; ++i) acc = __dadd_rn(acc, sq[i]);
+        const double acc = ordered_sum(sq, n);
         const double s = __dsqrt_rn(acc);
         nrm = s;
         if (cl.block_rank() == 0) hopm_record_norm(f, s);

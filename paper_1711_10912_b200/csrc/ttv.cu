@@ -444,12 +444,33 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
                 const TA *row = data + j * pitch + k0;
                 if constexpr (PAIRS) {
                     if (kn == kSmallSlab) {
+                        // the next 8 pairs load while the current 8 fold:
+                        // shared-memory latency stays off the add chain
+                        double2 cv[4], cb[4], nv[4], nb[4];
 #pragma unroll
-                        for (int kk = 0; kk < kSmallSlab; kk += 2) {
-                            const double2 v = *(const double2 *)(row + kk);
-                            const double2 bv = *(const double2 *)(bs + k0 + kk);
-                            acc = fold_step(acc, (Acc)v.x, bv.x);
-                            acc = fold_step(acc, (Acc)v.y, bv.y);
+                        for (int q = 0; q < 4; ++q) {
+                            cv[q] = *(const double2 *)(row + 2 * q);
+                            cb[q] = *(const double2 *)(bs + k0 + 2 * q);
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < kSmallSlab; kk += 8) {
+                            if (kk + 8 < kSmallSlab) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    nv[q] = *(const double2 *)(row + kk + 8 + 2 * q);
+                                    nb[q] = *(const double2 *)(bs + k0 + kk + 8 + 2 * q);
+                                }
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                acc = fold_step(acc, (Acc)cv[q].x, cb[q].x);
+                                acc = fold_step(acc, (Acc)cv[q].y, cb[q].y);
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                cv[q] = nv[q];
+                                cb[q] = nb[q];
+                            }
                         }
                     } else {
                         int kk = 0;
@@ -474,8 +495,31 @@ __global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ 
             } else {
                 const TA *col = data + k0 * 32 + j;
                 if (kn == kSmallSlab) {
+                    // next 8 terms load while the current 8 fold
+                    TA cx[8], nx[8];
+                    Acc cb[8], nb[8];
 #pragma unroll
-                    for (int kk = 0; kk < kSmallSlab; ++kk) acc = fold_step(acc, (Acc)col[kk * 32], bs[k0 + kk]);
+                    for (int q = 0; q < 8; ++q) {
+                        cx[q] = col[q * 32];
+                        cb[q] = bs[k0 + q];
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < kSmallSlab; kk += 8) {
+                        if (kk + 8 < kSmallSlab) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                nx[q] = col[(kk + 8 + q) * 32];
+                                nb[q] = bs[k0 + kk + 8 + q];
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc = fold_step(acc, (Acc)cx[q], cb[q]);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            cx[q] = nx[q];
+                            cb[q] = nb[q];
+                        }
+                    }
                 } else {
 #pragma unroll 8
                     for (int kk = 0; kk < kn; ++kk) acc = fold_step(acc, (Acc)col[kk * 32], bs[k0 + kk]);

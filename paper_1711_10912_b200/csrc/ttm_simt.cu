@@ -437,6 +437,187 @@ __global__ void __launch_bounds__(256) ttm_bulk_kernel(const __grid_constant__ T
     if (threadIdx.x == 0) bulk_wait<0>();
 }
 
+// float64, few rows J, output in A's order (ident): warp-specialised stream.
+// One persistent CTA per SM.  A producer warp keeps a ring of S tile slots
+// filled with 1-D TMA bulk copies (full / empty mbarrier per slot), and each
+// of NW consumer warps owns whole tiles (local tiles w, w + NW, ...): DMMA
+// over the tile's R*I positions (NT n8 tiles), fragments parked in the
+// warp's own double-buffered output tile, one bulk store per tile.  No
+// CTA-wide barrier in the steady state, and up to S tiles of A in flight per
+// SM -- the 2-stage bulk kernel keeps one tile in flight per CTA, too few
+// bytes for an HBM-bound stream of short tiles (config 5: 6 KB per tile).
+// Same per-element arithmetic as the other DMMA kernels (k-ordered FMA).
+constexpr int kStreamMaxSlots = 32;
+constexpr int kStreamMaxWarps = 8;
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(const __grid_constant__ TtmSimtParams P,
+                                                                              int S) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[kStreamMaxSlots], empty_bar[kStreamMaxSlots];
+    const int64_t K = P.K, I = P.I, J = P.J;
+    const int64_t KI = K * I;
+    const int64_t jpad = ttm_jpad(J);
+    const int ldb = (int)ttm_ldb(K);
+    const int NW = (int)(blockDim.x >> 5) - 1;
+    double *bsm = (double *)smem_raw;
+    unsigned char *slots = smem_raw + StagedLayout<double, true>(J, K).bbytes;
+    const size_t slot_bytes = ((size_t)P.R * KI * 8 + 15) & ~(size_t)15;
+    const size_t otile = ((size_t)P.R * J * I * 8 + 15) & ~(size_t)15;
+    unsigned char *outs = slots + (size_t)S * slot_bytes;
+
+    for (int64_t e = threadIdx.x; e < jpad * ldb; e += blockDim.x) {
+        const int64_t j = e / ldb, k = e - j * ldb;
+        bsm[e] = (j < J && k < K) ? ((const double *)P.bm)[j * P.bs0 + k * P.bs1] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NW) {
+        // producer: local tile q goes to slot q mod S once its previous
+        // occupant (tile q - S) has been released by its consumer warp
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;  // parity of the slot's previous release
+            for (int64_t q = 0; q < my_tiles; ++q) {
+                if (q >= S) mbar_wait_parity(&empty_bar[s], ph);
+                const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
+                const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
+                const uint32_t bytes = (uint32_t)(rows * KI * 8);
+                const uint32_t b16 = bytes & ~15u;
+                unsigned char *dst = slots + s * slot_bytes;
+                const unsigned char *src = (const unsigned char *)((const double *)P.a + o0 * KI);
+                // an 8-byte tail (last tile, odd R*K*I) is copied here; the
+                // arrive below releases it to the consumer
+                if (bytes != b16) *(double *)(dst + b16) = *(const double *)(src + b16);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&full_bar[s], b16);
+                if (b16) bulk_g2s(dst, src, b16, &full_bar[s]);
+                if (++s == S) {
+                    s = 0;
+                    if (q >= S) ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // consumer warp: fixed per-lane fragment geometry over the tile's positions
+    const int g = lane >> 2, t = lane & 3;
+    int base[NT], posb[NT];
+    int orow[NT][2], ooff[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        uint32_t r, i;
+        posb[nt] = nt * 8 + g;
+        P.I_div.divmod((uint32_t)posb[nt], r, i);
+        base[nt] = (int)(r * KI + i);
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            P.I_div.divmod((uint32_t)(nt * 8 + 2 * t + v), r, i);
+            orow[nt][v] = (int)r;  // >= rows for positions past the tile: skipped
+            ooff[nt][v] = (int)(r * J * I + i);
+        }
+    }
+    const double *brow = bsm + g * ldb + t;
+    const int Ki = (int)K, Ii = (int)I, Ji = (int)J;
+    const int Kfull = Ki & ~3;  // k-steps with all four k in range
+    const bool jfull = Ji == 16 * MT;
+    int parity_out = 0;
+    int s = warp % S;                            // slot of local tile q
+    uint32_t par = (uint32_t)((warp / S) & 1);  // its fill parity
+    for (int64_t q = warp; q < my_tiles; q += NW) {
+        mbar_wait_parity(&full_bar[s], par);
+        const double *st = (const double *)(slots + s * slot_bytes);
+        const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
+        const int rows = (int)(P.O - o0 < P.R ? P.O - o0 : P.R);
+        const int lim = rows * Ii;
+        bool pok[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) pok[nt] = posb[nt] < lim;
+
+        double acc[MT][NT][4];
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int b = 0; b < NT; ++b)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+        auto kstep = [&](int k4, bool kok) {
+            const int k = k4 + t;
+            double bf[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) bf[nt] = (pok[nt] && kok) ? st[base[nt] + k * Ii] : 0.0;
+#pragma unroll
+            for (int mm = 0; mm < MT; ++mm) {
+                const double a0 = brow[(mm * 16) * ldb + k4], a1 = brow[(mm * 16 + 8) * ldb + k4];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
+            }
+        };
+#pragma unroll 2
+        for (int k4 = 0; k4 < Kfull; k4 += 4) kstep(k4, true);
+        if (Kfull < Ki) kstep(Kfull, Kfull + t < Ki);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);  // the slot is free for tile q + S
+        s += NW;
+        while (s >= S) {
+            s -= S;
+            par ^= 1u;
+        }
+
+        double *ot = (double *)(outs + ((size_t)warp * 2 + parity_out) * otile);
+        parity_out ^= 1;
+        if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has been read out
+        __syncwarp();
+        if (rows == P.R && jfull) {
+            // whole tile, J fills the m16 tiles: only positions past R*I are skipped
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+#pragma unroll
+                    for (int mm = 0; mm < MT; ++mm)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            if (orow[nt][v] < P.R) ot[ooff[nt][v] + (mm * 16 + g + 8 * h) * Ii] = acc[mm][nt][2 * h + v];
+        } else {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    if (orow[nt][v] >= rows) continue;
+#pragma unroll
+                    for (int mm = 0; mm < MT; ++mm)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int j = mm * 16 + g + 8 * h;
+                            if (j < Ji) ot[ooff[nt][v] + j * Ii] = acc[mm][nt][2 * h + v];
+                        }
+                }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)(rows * J * I * 8);
+            const uint32_t b16 = bytes & ~15u;
+            double *dst = (double *)P.c + o0 * J * I;
+            if (b16) bulk_s2g(dst, ot, b16);
+            bulk_commit();
+            if (bytes != b16) dst[b16 / 8] = ot[b16 / 8];
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
 static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                          int m0, TtmSimtParams &P) {
     const int64_t J = bm.extent[0];
@@ -495,6 +676,72 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
         const char *e = getenv("TL_TTM_BULK_ST");
         return e ? atoi(e) : 2;  // measured: 2 stages (more CTAs per SM) beat 3-4
     }();
+    static const int64_t stream_kb = [] {
+        const char *e = getenv("TL_TTM_STREAM_KB");
+        return (int64_t)(e ? atoi(e) : 12);  // tile target; 0 disables the stream kernel
+    }();
+    static const int stream_nw = [] {
+        const char *e = getenv("TL_TTM_STREAM_NW");
+        const int v = e ? atoi(e) : kStreamMaxWarps;
+        return std::max(1, std::min(kStreamMaxWarps, v));
+    }();
+    if (a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0 && stream_kb > 0) {
+        // R: tile positions R*I fill whole n8 tiles as far as possible (at
+        // most 5 per warp for J <= 16, 4 for J <= 32: measured best); tile <= the target;
+        // tile starts 16-byte aligned in A and C
+        const int ntmax = P.J <= 16 ? 5 : 4;
+        int64_t bestR = 0;
+        double best_eff = 0.0;
+        for (int64_t R = 1; R * P.I <= 8 * ntmax && R * KI * 8 <= stream_kb * 1024; ++R) {
+            if ((R * KI) % 2 != 0 || (R * P.J * P.I) % 2 != 0) continue;
+            const int64_t pos = R * P.I;
+            const double eff = (double)pos / (double)(8 * ((pos + 7) / 8));
+            if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR)) {
+                best_eff = eff;
+                bestR = R;
+            }
+        }
+        if (bestR > 0 && best_eff >= 0.75) {
+            const int64_t R = bestR;
+            const int nt = (int)((R * P.I + 7) / 8);
+            const size_t bbytes = StagedLayout<double, true>(P.J, P.K).bbytes;
+            const size_t slot_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
+            const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
+            const size_t fixed = bbytes + (size_t)stream_nw * 2 * otile;
+            const size_t budget = 200 * 1024;
+            const int S = fixed < budget ? (int)std::min<size_t>(kStreamMaxSlots, (budget - fixed) / slot_bytes) : 0;
+            if (S >= 4) {
+                P.R = (int32_t)R;
+                P.ntiles = (P.O + R - 1) / R;
+                P.I_div.init((uint32_t)P.I);
+                const size_t smem = fixed + (size_t)S * slot_bytes;
+                const DeviceInfo &di = device_info();
+                const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms);
+                const int threads = 32 * (stream_nw + 1);
+                auto go = [&](auto kern) -> int {
+                    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    if (e != cudaSuccess) return cuda_status(e, "ttm stream smem");
+                    kern<<<(unsigned)grid, threads, smem, st>>>(P, S);
+                    return cuda_status(cudaGetLastError(), "ttm stream launch");
+                };
+                if (P.J <= 16) {
+                    switch (nt) {
+                        case 1: return go(ttm_stream_kernel<1, 1>);
+                        case 2: return go(ttm_stream_kernel<1, 2>);
+                        case 3: return go(ttm_stream_kernel<1, 3>);
+                        case 4: return go(ttm_stream_kernel<1, 4>);
+                        default: return go(ttm_stream_kernel<1, 5>);
+                    }
+                }
+                switch (nt) {
+                    case 1: return go(ttm_stream_kernel<2, 1>);
+                    case 2: return go(ttm_stream_kernel<2, 2>);
+                    case 3: return go(ttm_stream_kernel<2, 3>);
+                    default: return go(ttm_stream_kernel<2, 4>);
+                }
+            }
+        }
+    }
     if (a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0 && bulk_kb > 0) {
         // bulk-epilogue DMMA kernel: tiles of R slabs, outputs leave by TMA
         const int nt = (bulk_nt == 1 || bulk_nt == 4) ? bulk_nt : 2;

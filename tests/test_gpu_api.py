@@ -105,6 +105,14 @@ def ttm_case(shape, layout, mode, J, blayout, dtype, seed):
     ((3, 33, 5, 17, 2, 64), (1, 2, 3, 4, 5, 6), 2, 16, (1, 2)),  # config-5 ttm shape (smaller)
     ((9, 300, 41), (1, 2, 3), 2, 32, (1, 2)),   # J = 32, K large: B image too big -> GETT
     ((200, 60, 3), (2, 1, 3), 1, 32, (1, 2)),   # J = 32 permuted output: staged direct stores
+    # warp-specialised stream kernel edges: partial last tile with an odd
+    # R*K*I (8-byte tails in and out), J in (16, 32], K < 4 and K % 4 != 0,
+    # fewer tiles than SMs and than consumer warps, contracted stride 1
+    ((40, 999), (1, 2), 1, 20, (1, 2)),
+    ((50, 3, 701), (1, 2, 3), 2, 9, (2, 1)),
+    ((3, 10, 2), (1, 2, 3), 2, 5, (1, 2)),
+    ((7, 13, 3, 301), (1, 2, 3, 4), 2, 17, (1, 2)),
+    ((3, 33, 5, 17, 2, 13), (1, 2, 3, 4, 5, 6), 2, 16, (1, 2)),
 ])
 def test_ttm_float64_paths(gpu, case):
     shape, layout, mode, J, blayout = case

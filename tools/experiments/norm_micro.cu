@@ -87,6 +87,117 @@ __global__ void __launch_bounds__(256) gs_kernel(const double *a, int64_t n, dou
     finish<COMBINE>(block_dd(t), partials, ticket, out);
 }
 
+
+// last CTA: one warp folds the partials (no second block-wide reduction)
+__device__ void finish_warp(DD cta, double *partials, unsigned *ticket, double *out) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = cta.hi;
+        partials[2 * blockIdx.x + 1] = cta.lo;
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ticket) : "memory");
+        last = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    DD v{0, 0};
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) {
+        two_sum_add(v, __ldcg(partials + 2 * i));
+        v.lo += __ldcg(partials + 2 * i + 1);
+    }
+    for (int d = 16; d; d >>= 1) {
+        DD o{__shfl_down_sync(~0u, v.hi, d), __shfl_down_sync(~0u, v.lo, d)};
+        two_sum_add(v, o.hi); v.lo += o.lo;
+    }
+    if (threadIdx.x == 0) { *out = sqrt(v.hi + v.lo); *ticket = 0; }
+}
+
+#include <cooperative_groups.h>
+// clusters of CL CTAs: rank 0 gathers the cluster's CTA sums through DSMEM,
+// only rank 0 writes a partial and takes a ticket
+template <int U, int CL>
+__global__ void __launch_bounds__(256) gs_cluster_kernel(const double *a, int64_t n, double *partials, unsigned *ticket, double *out) {
+    namespace cg = cooperative_groups;
+    __shared__ DD mine;
+    __shared__ bool last;
+    double s[4] = {0, 0, 0, 0};
+    const int64_t nv = n / 2, nt = (int64_t)gridDim.x * blockDim.x;
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; v + (U - 1) * nt < nv; v += U * nt) {
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = __ldcs((const double2 *)a + v + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u) { s[(2 * u) & 3] = fma(x[u].x, x[u].x, s[(2 * u) & 3]); s[(2 * u + 1) & 3] = fma(x[u].y, x[u].y, s[(2 * u + 1) & 3]); }
+    }
+    {
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = (v + u * nt < nv) ? __ldcs((const double2 *)a + v + u * nt) : make_double2(0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) { s[(2 * u) & 3] = fma(x[u].x, x[u].x, s[(2 * u) & 3]); s[(2 * u + 1) & 3] = fma(x[u].y, x[u].y, s[(2 * u + 1) & 3]); }
+    }
+    DD t{s[0], 0};
+    two_sum_add(t, s[1]); two_sum_add(t, s[2]); two_sum_add(t, s[3]);
+    t = block_dd(t);
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) mine = t;
+    cl.sync();
+    if (cl.block_rank() == 0) {
+        if (threadIdx.x == 0) {
+            DD c{0, 0};
+            for (int r = 0; r < CL; ++r) {
+                const DD *o = cl.map_shared_rank(&mine, r);
+                two_sum_add(c, o->hi); c.lo += o->lo;
+            }
+            const int idx = blockIdx.x / CL, ncl = gridDim.x / CL;
+            partials[2 * idx] = c.hi;
+            partials[2 * idx + 1] = c.lo;
+            unsigned prev;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ticket) : "memory");
+            last = prev == ncl - 1;
+        }
+    }
+    cl.sync();  // others keep their smem alive until rank 0 has read it
+    if (cl.block_rank() != 0) return;
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    DD w{0, 0};
+    for (int i = threadIdx.x; i < (int)(gridDim.x / CL); i += 32) {
+        two_sum_add(w, __ldcg(partials + 2 * i));
+        w.lo += __ldcg(partials + 2 * i + 1);
+    }
+    for (int d = 16; d; d >>= 1) {
+        DD o{__shfl_down_sync(~0u, w.hi, d), __shfl_down_sync(~0u, w.lo, d)};
+        two_sum_add(w, o.hi); w.lo += o.lo;
+    }
+    if (threadIdx.x == 0) { *out = sqrt(w.hi + w.lo); *ticket = 0; }
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) gs_warpfin_kernel(const double *a, int64_t n, double *partials, unsigned *ticket, double *out) {
+    double s[4] = {0, 0, 0, 0};
+    const int64_t nv = n / 2, nt = (int64_t)gridDim.x * blockDim.x;
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; v + (U - 1) * nt < nv; v += U * nt) {
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = __ldcs((const double2 *)a + v + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u) { s[(2 * u) & 3] = fma(x[u].x, x[u].x, s[(2 * u) & 3]); s[(2 * u + 1) & 3] = fma(x[u].y, x[u].y, s[(2 * u + 1) & 3]); }
+    }
+    {
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = (v + u * nt < nv) ? __ldcs((const double2 *)a + v + u * nt) : make_double2(0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) { s[(2 * u) & 3] = fma(x[u].x, x[u].x, s[(2 * u) & 3]); s[(2 * u + 1) & 3] = fma(x[u].y, x[u].y, s[(2 * u + 1) & 3]); }
+    }
+    DD t{s[0], 0};
+    two_sum_add(t, s[1]); two_sum_add(t, s[2]); two_sum_add(t, s[3]);
+    finish_warp(block_dd(t), partials, ticket, out);
+}
+
 // V2: contiguous chunk per CTA, all of it requested up front by TMA bulk
 // copies (PIECE bytes each, one mbarrier per piece), reduced from smem.
 template <int PIECE, int NP>
@@ -183,6 +294,19 @@ int main(int argc, char **argv) {
         }
         report("gs U16 4/SM x256", [&] { gs_kernel<16, true><<<sms * 4, 256, 0, st>>>(a, n, parts, ticket, out); });
         report("gs U8 4/SM nocombine", [&] { gs_kernel<8, false><<<sms * 4, 256, 0, st>>>(a, n, parts, ticket, out); });
+        report("gs U8 4/SM warp-final", [&] { gs_warpfin_kernel<8><<<sms * 4, 256, 0, st>>>(a, n, parts, ticket, out); });
+        {
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 4; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(sms * 4); cfg.blockDim = dim3(256); cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
+            report("gs U8 4/SM cluster4", [&] { CK(cudaLaunchKernelEx(&cfg, gs_cluster_kernel<8, 4>, (const double *)a, n, parts, ticket, out)); });
+            cudaLaunchConfig_t cfg8 = cfg;
+            cudaLaunchAttribute at8[1] = {at[0]};
+            at8[0].val.clusterDim.x = 8; cfg8.attrs = at8;
+            report("gs U8 4/SM cluster8", [&] { CK(cudaLaunchKernelEx(&cfg8, gs_cluster_kernel<8, 8>, (const double *)a, n, parts, ticket, out)); });
+        }
         report("gs U4 8/SM x256", [&] { gs_kernel<4, true><<<sms * 8, 256, 0, st>>>(a, n, parts, ticket, out); });
         {
             auto k = bulk_kernel<16384, 13>;

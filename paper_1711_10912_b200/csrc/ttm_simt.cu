@@ -438,21 +438,26 @@ __global__ void __launch_bounds__(256) ttm_bulk_kernel(const __grid_constant__ T
 }
 
 // float64, few rows J, output in A's order (ident): warp-specialised stream.
-// One persistent CTA per SM.  A producer warp keeps a ring of S tile slots
-// filled with 1-D TMA bulk copies (full / empty mbarrier per slot), and each
-// of NW consumer warps owns whole tiles (local tiles w, w + NW, ...): DMMA
-// over the tile's R*I positions (NT n8 tiles), fragments parked in the
-// warp's own double-buffered output tile, one bulk store per tile.  No
-// CTA-wide barrier in the steady state, and up to S tiles of A in flight per
-// SM -- the 2-stage bulk kernel keeps one tile in flight per CTA, too few
-// bytes for an HBM-bound stream of short tiles (config 5: 6 KB per tile).
+// One persistent CTA per SM.  A producer thread keeps every consumer warp's
+// private ring of SW tile slots filled with 1-D TMA bulk copies (full / empty
+// mbarrier per slot); consumer warp w owns the CTA's local tiles w, w + NW,
+// w + 2 NW, ... (its j-th tile sits in slot w*SW + j mod SW): DMMA over the
+// tile's R*I positions (NT n8 tiles), fragments parked in the warp's own
+// double-buffered output tile, one bulk store per tile.  No CTA-wide barrier
+// in the steady state, and up to NW*SW tiles of A in flight per SM -- the
+// 2-stage bulk kernel keeps one tile in flight per CTA, too few bytes for an
+// HBM-bound stream of short tiles (config 5: 6 KB per tile).
+// Private rings keep every barrier wait unambiguous: a slot's successive
+// phases are waited on by one warp (and by the producer) strictly in order,
+// so no waiter ever asks for a phase two ahead of the barrier (an mbarrier
+// parity wait cannot tell phase n+2 from phase n).
 // Same per-element arithmetic as the other DMMA kernels (k-ordered FMA).
 constexpr int kStreamMaxSlots = 32;
 constexpr int kStreamMaxWarps = 8;
 
 template <int MT, int NT>
 __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(const __grid_constant__ TtmSimtParams P,
-                                                                              int S) {
+                                                                              int SW) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[kStreamMaxSlots], empty_bar[kStreamMaxSlots];
     const int64_t K = P.K, I = P.I, J = P.J;
@@ -460,6 +465,7 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
     const int64_t jpad = ttm_jpad(J);
     const int ldb = (int)ttm_ldb(K);
     const int NW = (int)(blockDim.x >> 5) - 1;
+    const int S = NW * SW;
     double *bsm = (double *)smem_raw;
     unsigned char *slots = smem_raw + StagedLayout<double, true>(J, K).bbytes;
     const size_t slot_bytes = ((size_t)P.R * KI * 8 + 15) & ~(size_t)15;
@@ -482,13 +488,15 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
     const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == NW) {
-        // producer: local tile q goes to slot q mod S once its previous
-        // occupant (tile q - S) has been released by its consumer warp
+        // producer: local tile q = w + NW*j goes to slot w*SW + j mod SW once
+        // that slot's previous tile (j - SW of warp w) has been released
         if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;  // parity of the slot's previous release
+            int w = 0, js = 0;
+            uint32_t jpar = 0;  // parity of fill j / SW
+            bool wrapped = false;  // j >= SW: the slot has a previous tile
             for (int64_t q = 0; q < my_tiles; ++q) {
-                if (q >= S) mbar_wait_parity(&empty_bar[s], ph);
+                const int s = w * SW + js;
+                if (wrapped) mbar_wait_parity(&empty_bar[s], jpar ^ 1u);
                 const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
                 const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
                 const uint32_t bytes = (uint32_t)(rows * KI * 8);
@@ -501,9 +509,13 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&full_bar[s], b16);
                 if (b16) bulk_g2s(dst, src, b16, &full_bar[s]);
-                if (++s == S) {
-                    s = 0;
-                    if (q >= S) ph ^= 1;
+                if (++w == NW) {
+                    w = 0;
+                    if (++js == SW) {
+                        js = 0;
+                        jpar ^= 1u;
+                        wrapped = true;
+                    }
                 }
             }
         }
@@ -519,7 +531,9 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
         uint32_t r, i;
         posb[nt] = nt * 8 + g;
         P.I_div.divmod((uint32_t)posb[nt], r, i);
-        base[nt] = (int)(r * KI + i);
+        // a position past the tile reads row 0 instead: its column of the
+        // product is never stored (DMMA columns are independent)
+        base[nt] = r < (uint32_t)P.R ? (int)(r * KI + i) : 0;
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
             P.I_div.divmod((uint32_t)(nt * 8 + 2 * t + v), r, i);
@@ -532,17 +546,14 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
     const int Kfull = Ki & ~3;  // k-steps with all four k in range
     const bool jfull = Ji == 16 * MT;
     int parity_out = 0;
-    int s = warp % S;                            // slot of local tile q
-    uint32_t par = (uint32_t)((warp / S) & 1);  // its fill parity
+    int js = 0;         // j mod SW for this warp's j-th tile
+    uint32_t jpar = 0;  // parity of fill j / SW
     for (int64_t q = warp; q < my_tiles; q += NW) {
-        mbar_wait_parity(&full_bar[s], par);
+        const int s = warp * SW + js;
+        mbar_wait_parity(&full_bar[s], jpar);
         const double *st = (const double *)(slots + s * slot_bytes);
         const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
         const int rows = (int)(P.O - o0 < P.R ? P.O - o0 : P.R);
-        const int lim = rows * Ii;
-        bool pok[NT];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) pok[nt] = posb[nt] < lim;
 
         double acc[MT][NT][4];
 #pragma unroll
@@ -551,11 +562,14 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
             for (int b = 0; b < NT; ++b)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+        // Positions past `rows` (partial last tile) fold stale slot data into
+        // columns that are never stored; only k >= K must read as zero
+        // (0 * stale could be NaN in a stored column).
         auto kstep = [&](int k4, bool kok) {
             const int k = k4 + t;
             double bf[NT];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) bf[nt] = (pok[nt] && kok) ? st[base[nt] + k * Ii] : 0.0;
+            for (int nt = 0; nt < NT; ++nt) bf[nt] = kok ? st[base[nt] + k * Ii] : 0.0;
 #pragma unroll
             for (int mm = 0; mm < MT; ++mm) {
                 const double a0 = brow[(mm * 16) * ldb + k4], a1 = brow[(mm * 16 + 8) * ldb + k4];
@@ -563,15 +577,14 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
                 for (int nt = 0; nt < NT; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
             }
         };
-#pragma unroll 2
+#pragma unroll 4
         for (int k4 = 0; k4 < Kfull; k4 += 4) kstep(k4, true);
         if (Kfull < Ki) kstep(Kfull, Kfull + t < Ki);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[s]);  // the slot is free for tile q + S
-        s += NW;
-        while (s >= S) {
-            s -= S;
-            par ^= 1u;
+        if (lane == 0) mbar_arrive(&empty_bar[s]);  // the slot is free for this warp's tile j + SW
+        if (++js == SW) {
+            js = 0;
+            jpar ^= 1u;
         }
 
         double *ot = (double *)(outs + ((size_t)warp * 2 + parity_out) * otile);
@@ -690,13 +703,23 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
         // most 5 per warp for J <= 16, 4 for J <= 32: measured best); tile <= the target;
         // tile starts 16-byte aligned in A and C
         const int ntmax = P.J <= 16 ? 5 : 4;
+        // Prefer tiles small enough for every consumer warp to keep two
+        // slots and two output tiles (measured: 5 warps with bigger tiles
+        // lose 20% at J = 32), then the fullest n8 tiles, then larger R.
+        const size_t bb = StagedLayout<double, true>(P.J, P.K).bbytes;
         int64_t bestR = 0;
         double best_eff = 0.0;
+        bool best_fit = false;
         for (int64_t R = 1; R * P.I <= 8 * ntmax && R * KI * 8 <= stream_kb * 1024; ++R) {
             if ((R * KI) % 2 != 0 || (R * P.J * P.I) % 2 != 0) continue;
             const int64_t pos = R * P.I;
             const double eff = (double)pos / (double)(8 * ((pos + 7) / 8));
-            if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR)) {
+            const size_t per_warp = 2 * (((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15) + 2 * (((size_t)R * KI * 8 + 15) & ~(size_t)15);
+            const bool fit = bb + (size_t)stream_nw * per_warp <= 200 * 1024;
+            const bool better = (fit != best_fit) ? fit
+                                : (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR));
+            if (bestR == 0 || better) {
+                best_fit = fit;
                 best_eff = eff;
                 bestR = R;
             }
@@ -707,21 +730,28 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
             const size_t bbytes = StagedLayout<double, true>(P.J, P.K).bbytes;
             const size_t slot_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
             const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
-            const size_t fixed = bbytes + (size_t)stream_nw * 2 * otile;
+            // NW consumer warps, each with SW >= 2 private slots and two
+            // output tiles; fewer warps when the smem budget demands it
             const size_t budget = 200 * 1024;
-            const int S = fixed < budget ? (int)std::min<size_t>(kStreamMaxSlots, (budget - fixed) / slot_bytes) : 0;
-            if (S >= 4) {
+            int nw = stream_nw, sw = 0;
+            for (; nw >= 2; --nw) {
+                const size_t per_warp = 2 * otile + 2 * slot_bytes;
+                if (bbytes + (size_t)nw * per_warp > budget) continue;
+                sw = (int)std::min<size_t>(kStreamMaxSlots / nw, (budget - bbytes - (size_t)nw * 2 * otile) / ((size_t)nw * slot_bytes));
+                break;
+            }
+            if (sw >= 2) {
                 P.R = (int32_t)R;
                 P.ntiles = (P.O + R - 1) / R;
                 P.I_div.init((uint32_t)P.I);
-                const size_t smem = fixed + (size_t)S * slot_bytes;
+                const size_t smem = bbytes + (size_t)nw * 2 * otile + (size_t)nw * sw * slot_bytes;
                 const DeviceInfo &di = device_info();
                 const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms);
-                const int threads = 32 * (stream_nw + 1);
+                const int threads = 32 * (nw + 1);
                 auto go = [&](auto kern) -> int {
                     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     if (e != cudaSuccess) return cuda_status(e, "ttm stream smem");
-                    kern<<<(unsigned)grid, threads, smem, st>>>(P, S);
+                    kern<<<(unsigned)grid, threads, smem, st>>>(P, sw);
                     return cuda_status(cudaGetLastError(), "ttm stream launch");
                 };
                 if (P.J <= 16) {

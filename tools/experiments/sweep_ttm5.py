@@ -3,6 +3,8 @@ import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))), "tests"))
 import numpy as np, torch
+import faulthandler
+faulthandler.dump_traceback_later(100, exit=True)
 import paper_1711_10912_b200 as tl
 import workloads as W
 

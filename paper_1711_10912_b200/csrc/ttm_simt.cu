@@ -452,7 +452,8 @@ __global__ void __launch_bounds__(256) ttm_bulk_kernel(const __grid_constant__ T
 // so no waiter ever asks for a phase two ahead of the barrier (an mbarrier
 // parity wait cannot tell phase n+2 from phase n).
 // Same per-element arithmetic as the other DMMA kernels (k-ordered FMA).
-constexpr int kStreamMaxSlots = 32;
+constexpr int kStreamMaxSlots = 48;
+constexpr size_t kStreamSmemBudget = 220 * 1024;  // one CTA per SM (227 KB max)
 constexpr int kStreamMaxWarps = 8;
 
 template <int MT, int NT>
@@ -715,7 +716,7 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
             const int64_t pos = R * P.I;
             const double eff = (double)pos / (double)(8 * ((pos + 7) / 8));
             const size_t per_warp = 2 * (((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15) + 2 * (((size_t)R * KI * 8 + 15) & ~(size_t)15);
-            const bool fit = bb + (size_t)stream_nw * per_warp <= 200 * 1024;
+            const bool fit = bb + (size_t)stream_nw * per_warp <= kStreamSmemBudget;
             const bool better = (fit != best_fit) ? fit
                                 : (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR));
             if (bestR == 0 || better) {
@@ -732,7 +733,7 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
             const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
             // NW consumer warps, each with SW >= 2 private slots and two
             // output tiles; fewer warps when the smem budget demands it
-            const size_t budget = 200 * 1024;
+            const size_t budget = kStreamSmemBudget;
             int nw = stream_nw, sw = 0;
             for (; nw >= 2; --nw) {
                 const size_t per_warp = 2 * otile + 2 * slot_bytes;

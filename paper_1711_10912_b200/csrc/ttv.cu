@@ -370,7 +370,7 @@ constexpr int kSmallSlab = 64;
 constexpr int kSmallMaxSlabs = 64;  // K <= 4096
 
 template <class TA, class TC, bool ROWS, bool PAIRS, bool CL = false>
-__global__ void __launch_bounds__(128) ttv_small_kernel(const __grid_constant__ TtvParams P) {
+__global__ void __launch_bounds__(256) ttv_small_kernel(const __grid_constant__ TtvParams P) {
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[kSmallMaxSlabs];
@@ -1336,7 +1336,15 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
         // few outputs: whole 32-output input blocks in flight, one fold warp
         L.regime = small_rows ? 3 : 2;
         L.grid = dim3((unsigned)(small_rows ? (P.O + 31) / 32 : P.O * ((P.I + 31) / 32)));
-        L.block = dim3(128);
+        // 7 copy warps + the fold warp: issuing the block's 16-byte cp.async
+        // copies is the fold's critical path with 3 (400^2 fold 7.3 -> 5.4 us;
+        // 384/512 threads measured slower again)
+        static const int small_threads = [] {
+            const char *e = getenv("TL_TTV_SMALL_THREADS");
+            const int v = e ? atoi(e) : 256;
+            return v == 128 || v == 256 ? v : 256;
+        }();
+        L.block = dim3(small_threads);
         // 16-byte element pairs for float64 when every pair is aligned and in range
         const bool pairs = (a.dtype == TL_F64) && (base % 16 == 0) && (small_rows ? (P.K % 2 == 0) : (P.I % 2 == 0));
         L.vec = pairs ? 2 : 1;

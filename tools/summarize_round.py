@@ -78,9 +78,14 @@ def raw(name):
     for r in rows[2:]:
         d = {"kernel": short(r[idx["Kernel Name"]])}
         for key in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-                    "sm__inst_executed_pipe_fp64.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"):
-            if key in idx:
-                v, u = r[idx[key]], units[idx[key]]
+                    "sm__inst_executed_pipe_fp64.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+                    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"):
+            col = idx.get(key)
+            if col is None:  # some sections prefix the metric name (e.g. "TPC.TriageCompute.")
+                col = next((i for h, i in idx.items() if h.endswith("." + key)), None)
+            if col is not None:
+                v, u = r[col], units[col]
                 try:
                     v = float(v.replace(",", ""))
                 except ValueError:
@@ -161,6 +166,17 @@ def main(tag):
                       f"{rd / 1e6 if rd else float('nan'):.1f} MB | {wr / 1e6 if wr else float('nan'):.1f} MB |")
             if name == "prof_ttv" and rd is not None and wr is not None:
                 ttv_dram.append(rd + wr)
+        for n, ((kid, k), m) in enumerate(det.items()):
+            r = rw[n] if n < len(rw) else {}
+            dm = r.get("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active")
+            tp = r.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
+            if dm:
+                extra = ""
+                t = r.get("gpu__time_duration.sum")
+                if name == "prof_ttm" and t:  # config-3 GETT: 2 * 512^3 * 384 flops per launch
+                    extra = f", {2 * 512 ** 3 * 384 / t / 1e12:.2f} FP64 TFLOP/s (cold, serialised)"
+                md.append(f"- id {kid} DMMA pipe: {dm:.1f}% of peak DMMA issue, tensor pipe active "
+                          f"{tp if tp is not None else float('nan'):.1f}% of elapsed{extra}")
         md.append("")
         for k, v in st.items():
             md.append(f"- `{k}` stalls: " + ", ".join(f"{c[6:]} {p}%" for c, p in v["stalls"].items()))

@@ -808,7 +808,8 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
                 kern<<<(unsigned)grid, threads, smem, st>>>(P);
                 return cuda_status(cudaGetLastError(), "ttm bulk launch");
             };
-            if (smem <= 200 * 1024) {
+            // one warp per 8*nt positions, at most the kernel's 256 threads
+            if (smem <= 200 * 1024 && threads <= 256) {
                 auto pick = [&](auto mt, auto ntc) -> int {
                     constexpr int MTv = decltype(mt)::value, NTv = decltype(ntc)::value;
                     if (nst == 2) return go(ttm_bulk_kernel<MTv, NTv, 2>);

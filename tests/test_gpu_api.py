@@ -113,6 +113,9 @@ def ttm_case(shape, layout, mode, J, blayout, dtype, seed):
     ((3, 10, 2), (1, 2, 3), 2, 5, (1, 2)),
     ((7, 13, 3, 301), (1, 2, 3, 4), 2, 17, (1, 2)),
     ((3, 33, 5, 17, 2, 13), (1, 2, 3, 4, 5, 6), 2, 16, (1, 2)),
+    # regression (wide fuzz): I = 256, J = 25 -- the bulk-epilogue fallback
+    # computed 512 threads for a 256-thread kernel (launch failed)
+    ((2, 8, 16, 7, 5, 2, 8), (1, 2, 3, 4, 5, 6, 7), 4, 25, (1, 2)),
 ])
 def test_ttm_float64_paths(gpu, case):
     shape, layout, mode, J, blayout = case

@@ -6,6 +6,7 @@ CPU oracle: bit-exact for ttv (all dtypes), int64 ttm and float32 ttm;
 float64 ttm within 1e-12 of sum|A||B|; inner/norm within the double-double
 bounds."""
 
+import os
 import random
 
 import numpy as np
@@ -15,6 +16,9 @@ import workloads as W
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
+
+# TL_FUZZ_SEEDS=N widens every sweep (default: the few seeds the suite runs)
+EXTRA = int(os.environ.get("TL_FUZZ_SEEDS", "0"))
 
 
 def tl():
@@ -43,7 +47,7 @@ def draw(nrng, shape, kind):
     return nrng.uniform(-1, 1, size=shape).astype(kind)
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(max(4, EXTRA)))
 def test_fuzz_ttv(gpu, seed):
     m = tl()
     rng, nrng = random.Random(100 + seed), np.random.default_rng(100 + seed)
@@ -64,7 +68,7 @@ def test_fuzz_ttv(gpu, seed):
         assert np.array_equal(bits(C), bits(want)), (shape, layout, mode, kind)
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(max(4, EXTRA)))
 def test_fuzz_ttm(gpu, seed):
     m = tl()
     rng, nrng = random.Random(200 + seed), np.random.default_rng(200 + seed)
@@ -92,7 +96,7 @@ def test_fuzz_ttm(gpu, seed):
             assert np.array_equal(bits(C), bits(want)), (shape, layout, mode, J, kind)
 
 
-@pytest.mark.parametrize("seed", range(2))
+@pytest.mark.parametrize("seed", range(max(2, EXTRA)))
 def test_fuzz_inner_norm(gpu, seed):
     m = tl()
     rng, nrng = random.Random(300 + seed), np.random.default_rng(300 + seed)
@@ -121,3 +125,27 @@ def test_fuzz_inner_norm(gpu, seed):
         nrm = m.frobenius_norm(A)
         wn = O.norm(ba, shape, sa)
         assert abs(nrm - wn) <= tol * wn + 1e-300, (shape, la)
+
+
+@pytest.mark.parametrize("seed", range(max(3, EXTRA)))
+def test_fuzz_ttm_small_j_first_order(gpu, seed):
+    """float64 ttm with J <= 32 on first-order tensors (outputs in A's order):
+    the warp-specialised stream kernel and its fallbacks, including partial
+    last tiles, odd R*K*I (8-byte tails) and tiny O."""
+    m = tl()
+    rng, nrng = random.Random(400 + seed), np.random.default_rng(400 + seed)
+    for t in range(30):
+        shape = rand_shape(rng, 2_000_000)
+        p = len(shape)
+        layout = tuple(range(1, p + 1))
+        mode = rng.randint(1, p)
+        J = rng.randint(1, 32)
+        T = nrng.standard_normal(shape)
+        M = nrng.standard_normal((J, shape[mode - 1]))
+        buf, mbuf = W.layout_buffer(T, layout), W.layout_buffer(M, (1, 2))
+        C = m.ttm(m.DenseTensor.from_memory(shape, buf, layout=layout),
+                  m.DenseTensor.from_memory(M.shape, mbuf), mode).numpy()
+        st, bst = W.compute_strides(shape, layout), W.compute_strides(M.shape, (1, 2))
+        want = O.ttm(buf, shape, st, mbuf, M.shape, bst, mode)
+        bound = O.ttm(np.abs(buf), shape, st, np.abs(mbuf), M.shape, bst, mode)
+        assert np.all(np.abs(C - want) <= 1e-12 * bound), (shape, mode, J)

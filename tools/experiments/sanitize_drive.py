@@ -21,6 +21,7 @@ G = T((48, 40, 36), (3, 2, 1)); M = tl.DenseTensor.from_memory((64, 40), rng.sta
 tl.ttm(G, M, 2)
 G32 = T((48, 40, 36), (1, 2, 3), np.float32); tl.ttm(G32, M.to(torch.float32), 2)
 Bk = T((5, 37, 201), (1, 2, 3)); tl.ttm(Bk, tl.DenseTensor.from_memory((16, 37), rng.standard_normal(16 * 37)), 2)
+St = T((40, 999), (1, 2)); tl.ttm(St, tl.DenseTensor.from_memory((20, 40), rng.standard_normal(20 * 40)), 1)  # stream, partial tile
 Sp = T((20, 33, 7), (2, 1, 3)); tl.ttm(Sp, tl.DenseTensor.from_memory((8, 33), rng.standard_normal(8 * 33)), 2)
 # reductions, copy, hopm
 tl.inner_product_tensors(A, A); tl.frobenius_norm(B); tl.frobenius_norm(G)

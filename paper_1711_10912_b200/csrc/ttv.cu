@@ -247,7 +247,7 @@ struct TtvBoxParams {
     int64_t rs_as[TL_MAX_DIGITS], rs_cs[TL_MAX_DIGITS];
 };
 
-template <class TA, class TC, int VEC, int NJ>
+template <class TA, class TC, int VEC, int NJ, int UB = 8>
 __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ TtvBoxParams P) {
     using Acc = typename AccOf<TA>::type;
     constexpr int BA = 32 * VEC, BC = 8 * NJ, PITCH = BA + 1;
@@ -312,8 +312,9 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
         const int a = lane * VEC;
         const bool a_ok = ab * BA + a + VEC <= P.e0;
         // NJ passes of 8 chain rows (one per warp); each pass is the strided
-        // kernel's k loop: U rows of VEC elements in flight per thread
-        constexpr int U = 8;
+        // kernel's k loop: U rows of VEC elements in flight per thread (U = K
+        // for K = 9: one round trip per pass instead of two)
+        constexpr int U = UB;
         for (int t = 0; t < NJ; ++t) {
             const int j = warp + 8 * t;
             const int64_t ta = tabA[j];
@@ -1062,6 +1063,10 @@ static cudaError_t launch_box(const TtvLaunch &L, cudaStream_t st) {
     if constexpr (sizeof(TA) == 4) {
         if (L.vec == 4) return go(ttv_box_kernel<TA, TC, 4, 8>);
     }
+    // K = 9: the whole fold in flight per pass (config 5 seed 5: 150.6 ->
+    // 147.2 us at the same 64 registers; K = 10..12 would need 69-78
+    // registers, one CTA per SM fewer, unmeasured)
+    if (L.vec == 2 && L.box.K == 9) return go(ttv_box_kernel<TA, TC, 2, 8, 9>);
     if (L.vec == 2) return go(ttv_box_kernel<TA, TC, 2, 8>);
     return go(ttv_box_kernel<TA, TC, 1, 8>);
 }

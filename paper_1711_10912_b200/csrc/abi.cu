@@ -42,6 +42,7 @@ int residual_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u
                      cudaStream_t st);
 int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len);
 int ttm_dmma_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out);
+int ttm_staged_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out);
 
 static thread_local std::string g_error = "no error";
 
@@ -394,12 +395,19 @@ int tl_plan_describe(int32_t op, const tl_desc *a, const tl_desc *bmat, int32_t 
         set_error("plan: matrix does not match mode %d", mode);
         return TL_EINVAL;
     }
+    // the dispatch order of tl_ttm
     std::string s;
-    int rc = bmat->extent[0] <= 32 ? TL_EUNSUPPORTED : ttm_dmma_describe(*a, *bmat, mode - 1, s);
+    const bool few_rows = bmat->extent[0] <= 32;
+    const bool fp = a->dtype == TL_F64 || a->dtype == TL_F32;
+    int rc = TL_EUNSUPPORTED;
+    if (few_rows || !fp) rc = ttm_staged_describe(*a, *bmat, mode - 1, s);
+    if (rc == TL_EUNSUPPORTED && fp) {
+        rc = ttm_dmma_describe(*a, *bmat, mode - 1, s);
+        if (rc == TL_EUNSUPPORTED && !few_rows) rc = ttm_staged_describe(*a, *bmat, mode - 1, s);
+    }
     if (rc == TL_EUNSUPPORTED) {
         const int64_t F = volume(*a) / a->extent[mode - 1];
-        s = std::string("{\"path\": \"") + (bmat->extent[0] <= 32 ? "staged" : "simt") + "\", \"F\": " +
-            std::to_string(F) + "}";
+        s = std::string("{\"path\": \"simt\", \"F\": ") + std::to_string(F) + "}";
         rc = TL_OK;
     }
     if (rc != TL_OK) return rc;

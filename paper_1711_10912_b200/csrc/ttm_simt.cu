@@ -15,6 +15,7 @@
 // ttm_simt: one thread per output, the reference's fold (fallback).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "plan.h"
@@ -659,171 +660,206 @@ static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm,
     return true;
 }
 
+// Tuning knobs of the small-J kernels (environment, read once).
+struct SmallTtmKnobs {
+    int64_t stage_kb = 28, bulk_kb = 14, stream_kb = 12;
+    int ntile = 4, bulk_nt = 2, bulk_st = 2, stream_nw = kStreamMaxWarps;
+    bool force_simt = false;
+};
+static const SmallTtmKnobs &small_ttm_knobs() {
+    static const SmallTtmKnobs k = [] {
+        SmallTtmKnobs v;
+        auto num = [](const char *name, int64_t dflt) {
+            const char *e = getenv(name);
+            return e ? (int64_t)atoll(e) : dflt;
+        };
+        v.stage_kb = num("TL_TTM_STAGE_KB", 28);
+        v.ntile = (int)num("TL_TTM_NT", 4);
+        v.force_simt = getenv("TL_TTM_SIMT") != nullptr;
+        v.bulk_kb = num("TL_TTM_BULK_KB", 14);
+        v.bulk_nt = (int)num("TL_TTM_BULK_NT", 2);
+        v.bulk_st = (int)num("TL_TTM_BULK_ST", 2);  // measured: 2 stages (more CTAs per SM) beat 3-4
+        v.stream_kb = num("TL_TTM_STREAM_KB", 12);  // tile target; 0 disables the stream kernel
+        v.stream_nw = (int)std::max<int64_t>(1, std::min<int64_t>(kStreamMaxWarps, num("TL_TTM_STREAM_NW", kStreamMaxWarps)));
+        return v;
+    }();
+    return k;
+}
+
+struct StreamPlan {
+    int64_t R = 0;
+    int nt = 0, nw = 0, sw = 0;
+    size_t smem = 0;
+};
+// Stream-kernel plan (host only).  R: tile positions R*I fill whole n8 tiles
+// as far as possible (at most 5 per warp for J <= 16, 4 for J <= 32:
+// measured best); tile <= the target; tile starts 16-byte aligned in A and C.
+// Prefer tiles small enough for every consumer warp to keep two slots and
+// two output tiles (measured: 5 warps with bigger tiles lose 20% at J = 32),
+// then the fullest n8 tiles, then larger R.
+static bool plan_stream(const TtmSimtParams &P, StreamPlan &sp) {
+    const SmallTtmKnobs &kn = small_ttm_knobs();
+    if (kn.stream_kb <= 0) return false;
+    const int64_t KI = P.K * P.I;
+    const int ntmax = P.J <= 16 ? 5 : 4;
+    const size_t bb = StagedLayout<double, true>(P.J, P.K).bbytes;
+    int64_t bestR = 0;
+    double best_eff = 0.0;
+    bool best_fit = false;
+    for (int64_t R = 1; R * P.I <= 8 * ntmax && R * KI * 8 <= kn.stream_kb * 1024; ++R) {
+        if ((R * KI) % 2 != 0 || (R * P.J * P.I) % 2 != 0) continue;
+        const int64_t pos = R * P.I;
+        const double eff = (double)pos / (double)(8 * ((pos + 7) / 8));
+        const size_t per_warp = 2 * (((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15) + 2 * (((size_t)R * KI * 8 + 15) & ~(size_t)15);
+        const bool fit = bb + (size_t)kn.stream_nw * per_warp <= kStreamSmemBudget;
+        const bool better = (fit != best_fit) ? fit : (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR));
+        if (bestR == 0 || better) {
+            best_fit = fit;
+            best_eff = eff;
+            bestR = R;
+        }
+    }
+    if (bestR == 0 || best_eff < 0.75) return false;
+    const size_t slot_bytes = ((size_t)bestR * KI * 8 + 15) & ~(size_t)15;
+    const size_t otile = ((size_t)bestR * P.J * P.I * 8 + 15) & ~(size_t)15;
+    // NW consumer warps, each with SW >= 2 private slots and two output
+    // tiles; fewer warps when the smem budget demands it
+    int nw = kn.stream_nw, sw = 0;
+    for (; nw >= 2; --nw) {
+        if (bb + (size_t)nw * (2 * otile + 2 * slot_bytes) > kStreamSmemBudget) continue;
+        sw = (int)std::min<size_t>(kStreamMaxSlots / nw, (kStreamSmemBudget - bb - (size_t)nw * 2 * otile) / ((size_t)nw * slot_bytes));
+        break;
+    }
+    if (sw < 2) return false;
+    sp.R = bestR;
+    sp.nt = (int)((bestR * P.I + 7) / 8);
+    sp.nw = nw;
+    sp.sw = sw;
+    sp.smem = bb + (size_t)nw * 2 * otile + (size_t)nw * sw * slot_bytes;
+    return true;
+}
+
+struct BulkPlan {
+    int64_t R = 0;
+    int nt = 0, nst = 0, threads = 0;
+    size_t smem = 0;
+};
+// Bulk-epilogue kernel plan (host only): tiles of R slabs, outputs leave by
+// TMA; R*I preferably a multiple of the 8*nt positions one warp owns.
+static bool plan_bulk(const TtmSimtParams &P, BulkPlan &bp) {
+    const SmallTtmKnobs &kn = small_ttm_knobs();
+    if (kn.bulk_kb <= 0) return false;
+    const int64_t KI = P.K * P.I;
+    const int nt = (kn.bulk_nt == 1 || kn.bulk_nt == 4) ? kn.bulk_nt : 2;
+    const int64_t rmax = std::max<int64_t>(1, std::min<int64_t>((64 * nt) / P.I, kn.bulk_kb * 1024 / (KI * 8)));
+    int64_t unit = 8 * nt;
+    for (int64_t d = P.I; d > 0;) {  // unit = 8 nt / gcd(I, 8 nt)
+        const int64_t r = unit % d;
+        unit = d;
+        d = r;
+    }
+    unit = 8 * nt / unit;
+    int64_t R = rmax / unit * unit;
+    if (R == 0 && unit * P.I <= 64 * nt && unit * KI * 8 <= 32 * 1024) R = unit;
+    if (R == 0) R = rmax;
+    while (R > 1 && ((R * KI * 8) % 16 != 0 || (R * P.J * P.I) % 2 != 0)) --R;
+    if ((R * KI * 8) % 16 != 0 || (R * P.J * P.I) % 2 != 0) return false;
+    const int threads = (int)(((R * P.I + 8 * nt - 1) / (8 * nt)) * 32);
+    const size_t stage_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
+    const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
+    const int nst = kn.bulk_st <= 2 ? 2 : (kn.bulk_st == 3 ? 3 : 4);
+    const size_t smem = StagedLayout<double, true>(P.J, P.K).bbytes + nst * stage_bytes + 2 * otile;
+    // one warp per 8*nt positions, at most the kernel's 256 threads
+    if (smem > 200 * 1024 || threads > 256) return false;
+    bp.R = R;
+    bp.nt = nt;
+    bp.nst = nst;
+    bp.threads = threads;
+    bp.smem = smem;
+    return true;
+}
+
+// Shared gate of the small-J staged family (I <= 256, a [K][I] block <= 32 KB,
+// B image <= 48 KB, 16-byte aligned A); false -> the caller uses another path.
+static bool staged_family_ok(const TtmSimtParams &P, int32_t dtype) {
+    const int64_t s = (int64_t)dtype_size(dtype);
+    return !(P.I > 256 || P.K * P.I * s > 32 * 1024 || P.J * P.K * 8 > 48 * 1024 || (uintptr_t)P.a % 16 != 0 ||
+             P.O > 0xffffffffll);
+}
+
 int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                        int m0, cudaStream_t st) {
     TtmSimtParams P{};
     if (!build_params(a, a_ptr, bm, b_ptr, c_ptr, m0, P)) return TL_EUNSUPPORTED;
     const int64_t s = (int64_t)dtype_size(a.dtype);
     const int64_t KI = P.K * P.I;
-    const uintptr_t base = (uintptr_t)P.a;
     if (P.O * P.I == 0) return TL_OK;
-    if (P.I > 256 || KI * s > 32 * 1024 || P.J * P.K * 8 > 48 * 1024 || base % 16 != 0 || P.O > 0xffffffffll)
-        return TL_EUNSUPPORTED;
-    static const int64_t stage_kb = [] {
-        const char *e = getenv("TL_TTM_STAGE_KB");
-        return (int64_t)(e ? atoi(e) : 28);
-    }();
-    static const int ntile = [] {
-        const char *e = getenv("TL_TTM_NT");
-        return e ? atoi(e) : 4;
-    }();
-    static const bool force_simt = getenv("TL_TTM_SIMT") != nullptr;
-    static const int64_t bulk_kb = [] {
-        const char *e = getenv("TL_TTM_BULK_KB");
-        return (int64_t)(e ? atoi(e) : 14);
-    }();
-    static const int bulk_nt = [] {
-        const char *e = getenv("TL_TTM_BULK_NT");
-        return e ? atoi(e) : 2;
-    }();
-    static const int bulk_st = [] {
-        const char *e = getenv("TL_TTM_BULK_ST");
-        return e ? atoi(e) : 2;  // measured: 2 stages (more CTAs per SM) beat 3-4
-    }();
-    static const int64_t stream_kb = [] {
-        const char *e = getenv("TL_TTM_STREAM_KB");
-        return (int64_t)(e ? atoi(e) : 12);  // tile target; 0 disables the stream kernel
-    }();
-    static const int stream_nw = [] {
-        const char *e = getenv("TL_TTM_STREAM_NW");
-        const int v = e ? atoi(e) : kStreamMaxWarps;
-        return std::max(1, std::min(kStreamMaxWarps, v));
-    }();
-    if (a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0 && stream_kb > 0) {
-        // R: tile positions R*I fill whole n8 tiles as far as possible (at
-        // most 5 per warp for J <= 16, 4 for J <= 32: measured best); tile <= the target;
-        // tile starts 16-byte aligned in A and C
-        const int ntmax = P.J <= 16 ? 5 : 4;
-        // Prefer tiles small enough for every consumer warp to keep two
-        // slots and two output tiles (measured: 5 warps with bigger tiles
-        // lose 20% at J = 32), then the fullest n8 tiles, then larger R.
-        const size_t bb = StagedLayout<double, true>(P.J, P.K).bbytes;
-        int64_t bestR = 0;
-        double best_eff = 0.0;
-        bool best_fit = false;
-        for (int64_t R = 1; R * P.I <= 8 * ntmax && R * KI * 8 <= stream_kb * 1024; ++R) {
-            if ((R * KI) % 2 != 0 || (R * P.J * P.I) % 2 != 0) continue;
-            const int64_t pos = R * P.I;
-            const double eff = (double)pos / (double)(8 * ((pos + 7) / 8));
-            const size_t per_warp = 2 * (((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15) + 2 * (((size_t)R * KI * 8 + 15) & ~(size_t)15);
-            const bool fit = bb + (size_t)stream_nw * per_warp <= kStreamSmemBudget;
-            const bool better = (fit != best_fit) ? fit
-                                : (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR));
-            if (bestR == 0 || better) {
-                best_fit = fit;
-                best_eff = eff;
-                bestR = R;
+    if (!staged_family_ok(P, a.dtype)) return TL_EUNSUPPORTED;
+    const SmallTtmKnobs &kn = small_ttm_knobs();
+    const int64_t stage_kb = kn.stage_kb;
+    const int ntile = kn.ntile;
+    const bool force_simt = kn.force_simt;
+    const bool dmma_ident = a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0;
+    StreamPlan sp;
+    if (dmma_ident && plan_stream(P, sp)) {
+        P.R = (int32_t)sp.R;
+        P.ntiles = (P.O + sp.R - 1) / sp.R;
+        P.I_div.init((uint32_t)P.I);
+        const DeviceInfo &di = device_info();
+        const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms);
+        const int threads = 32 * (sp.nw + 1);
+        const size_t smem = sp.smem;
+        const int sw = sp.sw;
+        auto go = [&](auto kern) -> int {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return cuda_status(e, "ttm stream smem");
+            kern<<<(unsigned)grid, threads, smem, st>>>(P, sw);
+            return cuda_status(cudaGetLastError(), "ttm stream launch");
+        };
+        if (P.J <= 16) {
+            switch (sp.nt) {
+                case 1: return go(ttm_stream_kernel<1, 1>);
+                case 2: return go(ttm_stream_kernel<1, 2>);
+                case 3: return go(ttm_stream_kernel<1, 3>);
+                case 4: return go(ttm_stream_kernel<1, 4>);
+                default: return go(ttm_stream_kernel<1, 5>);
             }
         }
-        if (bestR > 0 && best_eff >= 0.75) {
-            const int64_t R = bestR;
-            const int nt = (int)((R * P.I + 7) / 8);
-            const size_t bbytes = StagedLayout<double, true>(P.J, P.K).bbytes;
-            const size_t slot_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
-            const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
-            // NW consumer warps, each with SW >= 2 private slots and two
-            // output tiles; fewer warps when the smem budget demands it
-            const size_t budget = kStreamSmemBudget;
-            int nw = stream_nw, sw = 0;
-            for (; nw >= 2; --nw) {
-                const size_t per_warp = 2 * otile + 2 * slot_bytes;
-                if (bbytes + (size_t)nw * per_warp > budget) continue;
-                sw = (int)std::min<size_t>(kStreamMaxSlots / nw, (budget - bbytes - (size_t)nw * 2 * otile) / ((size_t)nw * slot_bytes));
-                break;
-            }
-            if (sw >= 2) {
-                P.R = (int32_t)R;
-                P.ntiles = (P.O + R - 1) / R;
-                P.I_div.init((uint32_t)P.I);
-                const size_t smem = bbytes + (size_t)nw * 2 * otile + (size_t)nw * sw * slot_bytes;
-                const DeviceInfo &di = device_info();
-                const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms);
-                const int threads = 32 * (nw + 1);
-                auto go = [&](auto kern) -> int {
-                    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    if (e != cudaSuccess) return cuda_status(e, "ttm stream smem");
-                    kern<<<(unsigned)grid, threads, smem, st>>>(P, sw);
-                    return cuda_status(cudaGetLastError(), "ttm stream launch");
-                };
-                if (P.J <= 16) {
-                    switch (nt) {
-                        case 1: return go(ttm_stream_kernel<1, 1>);
-                        case 2: return go(ttm_stream_kernel<1, 2>);
-                        case 3: return go(ttm_stream_kernel<1, 3>);
-                        case 4: return go(ttm_stream_kernel<1, 4>);
-                        default: return go(ttm_stream_kernel<1, 5>);
-                    }
-                }
-                switch (nt) {
-                    case 1: return go(ttm_stream_kernel<2, 1>);
-                    case 2: return go(ttm_stream_kernel<2, 2>);
-                    case 3: return go(ttm_stream_kernel<2, 3>);
-                    default: return go(ttm_stream_kernel<2, 4>);
-                }
-            }
+        switch (sp.nt) {
+            case 1: return go(ttm_stream_kernel<2, 1>);
+            case 2: return go(ttm_stream_kernel<2, 2>);
+            case 3: return go(ttm_stream_kernel<2, 3>);
+            default: return go(ttm_stream_kernel<2, 4>);
         }
     }
-    if (a.dtype == TL_F64 && P.J <= 32 && P.ident && !force_simt && (uintptr_t)c_ptr % 16 == 0 && bulk_kb > 0) {
-        // bulk-epilogue DMMA kernel: tiles of R slabs, outputs leave by TMA
-        const int nt = (bulk_nt == 1 || bulk_nt == 4) ? bulk_nt : 2;
-        const int64_t rmax = std::max<int64_t>(1, std::min<int64_t>((64 * nt) / P.I, bulk_kb * 1024 / (KI * 8)));
-        // prefer R with R*I a multiple of the 8*nt positions one warp owns
-        // (no idle MMA columns), even if that overshoots the stage target
-        int64_t unit = 8 * nt;
-        for (int64_t d = P.I; d > 0;) {  // unit = 8 nt / gcd(I, 8 nt)
-            const int64_t r = unit % d;
-            unit = d;
-            d = r;
-        }
-        unit = 8 * nt / unit;
-        int64_t R = rmax / unit * unit;
-        if (R == 0 && unit * P.I <= 64 * nt && unit * KI * 8 <= 32 * 1024) R = unit;
-        if (R == 0) R = rmax;
-        while (R > 1 && ((R * KI * 8) % 16 != 0 || (R * P.J * P.I) % 2 != 0)) --R;
-        if ((R * KI * 8) % 16 == 0 && (R * P.J * P.I) % 2 == 0) {
-            P.R = (int32_t)R;
-            P.ntiles = (P.O + R - 1) / R;
-            P.I_div.init((uint32_t)P.I);
-            const int threads = (int)(((R * P.I + 8 * nt - 1) / (8 * nt)) * 32);
-            const size_t stage_bytes = ((size_t)R * KI * 8 + 15) & ~(size_t)15;
-            const size_t otile = ((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15;
-            const int nst = bulk_st <= 2 ? 2 : (bulk_st == 3 ? 3 : 4);
-            const size_t smem = StagedLayout<double, true>(P.J, P.K).bbytes + nst * stage_bytes + 2 * otile;
-            const DeviceInfo &di = device_info();
-            const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (228 * 1024) / (int64_t)(smem + 2048)));
-            const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * per_sm);
-            auto go = [&](auto kern) -> int {
-                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                if (e != cudaSuccess) return cuda_status(e, "ttm bulk smem");
-                kern<<<(unsigned)grid, threads, smem, st>>>(P);
-                return cuda_status(cudaGetLastError(), "ttm bulk launch");
-            };
-            // one warp per 8*nt positions, at most the kernel's 256 threads
-            if (smem <= 200 * 1024 && threads <= 256) {
-                auto pick = [&](auto mt, auto ntc) -> int {
-                    constexpr int MTv = decltype(mt)::value, NTv = decltype(ntc)::value;
-                    if (nst == 2) return go(ttm_bulk_kernel<MTv, NTv, 2>);
-                    if (nst == 3) return go(ttm_bulk_kernel<MTv, NTv, 3>);
-                    return go(ttm_bulk_kernel<MTv, NTv, 4>);
-                };
-                using I1 = std::integral_constant<int, 1>;
-                using I2 = std::integral_constant<int, 2>;
-                using I4 = std::integral_constant<int, 4>;
-                if (nt == 1) return P.J <= 16 ? pick(I1{}, I1{}) : pick(I2{}, I1{});
-                if (nt == 2) return P.J <= 16 ? pick(I1{}, I2{}) : pick(I2{}, I2{});
-                return P.J <= 16 ? pick(I1{}, I4{}) : pick(I2{}, I4{});
-            }
-        }
+    BulkPlan bp;
+    if (dmma_ident && plan_bulk(P, bp)) {
+        P.R = (int32_t)bp.R;
+        P.ntiles = (P.O + bp.R - 1) / bp.R;
+        P.I_div.init((uint32_t)P.I);
+        const DeviceInfo &di = device_info();
+        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (228 * 1024) / (int64_t)(bp.smem + 2048)));
+        const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * per_sm);
+        const int threads = bp.threads;
+        const size_t smem = bp.smem;
+        auto go = [&](auto kern) -> int {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return cuda_status(e, "ttm bulk smem");
+            kern<<<(unsigned)grid, threads, smem, st>>>(P);
+            return cuda_status(cudaGetLastError(), "ttm bulk launch");
+        };
+        auto pick = [&](auto mt, auto ntc) -> int {
+            constexpr int MTv = decltype(mt)::value, NTv = decltype(ntc)::value;
+            if (bp.nst == 2) return go(ttm_bulk_kernel<MTv, NTv, 2>);
+            if (bp.nst == 3) return go(ttm_bulk_kernel<MTv, NTv, 3>);
+            return go(ttm_bulk_kernel<MTv, NTv, 4>);
+        };
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        using I4 = std::integral_constant<int, 4>;
+        if (bp.nt == 1) return P.J <= 16 ? pick(I1{}, I1{}) : pick(I2{}, I1{});
+        if (bp.nt == 2) return P.J <= 16 ? pick(I1{}, I2{}) : pick(I2{}, I2{});
+        return P.J <= 16 ? pick(I1{}, I4{}) : pick(I2{}, I4{});
     }
     const int64_t stage_target = stage_kb * 1024;
     int64_t R = std::max<int64_t>(1, std::min<int64_t>(256 / P.I, stage_target / (KI * s)));
@@ -860,6 +896,38 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
     if (a.dtype == TL_F64) return go(ttm_staged_kernel<double, 0>);
     if (a.dtype == TL_F32) return go(ttm_staged_kernel<float, 0>);
     return go(ttm_staged_kernel<int64_t, 0>);
+}
+
+// Which small-J kernel a ttm with J <= 32 would use (host only; outputs are
+// freshly allocated, so C is taken as 16-byte aligned).  TL_EUNSUPPORTED: the
+// staged family does not apply (the caller falls back to the GETT / SIMT path).
+int ttm_staged_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out) {
+    TtmSimtParams P{};
+    if (!build_params(a, (const void *)0x100000, bm, (const void *)0x200000, (void *)0x300000, m0, P))
+        return TL_EUNSUPPORTED;
+    if (!staged_family_ok(P, a.dtype)) return TL_EUNSUPPORTED;
+    const SmallTtmKnobs &kn = small_ttm_knobs();
+    const bool dmma_ident = a.dtype == TL_F64 && P.J <= 32 && P.ident && !kn.force_simt;
+    const std::string head = "{\"O\": " + std::to_string(P.O) + ", \"K\": " + std::to_string(P.K) + ", \"I\": " +
+                             std::to_string(P.I) + ", \"J\": " + std::to_string(P.J) + ", ";
+    StreamPlan sp;
+    BulkPlan bp;
+    if (dmma_ident && plan_stream(P, sp)) {
+        out = head + "\"path\": \"stream\", \"R\": " + std::to_string(sp.R) + ", \"NT\": " + std::to_string(sp.nt) +
+              ", \"warps\": " + std::to_string(sp.nw) + ", \"slots_per_warp\": " + std::to_string(sp.sw) +
+              ", \"smem\": " + std::to_string(sp.smem) + "}";
+    } else if (dmma_ident && plan_bulk(P, bp)) {
+        out = head + "\"path\": \"bulk\", \"R\": " + std::to_string(bp.R) + ", \"threads\": " +
+              std::to_string(bp.threads) + ", \"smem\": " + std::to_string(bp.smem) + "}";
+    } else {
+        // the staged kernel's own tile constraint (ttm_staged_enqueue)
+        const int64_t s = (int64_t)dtype_size(a.dtype), KI = P.K * P.I;
+        int64_t R = std::max<int64_t>(1, std::min<int64_t>(256 / P.I, kn.stage_kb * 1024 / (KI * s)));
+        while (R > 1 && (R * KI * s) % 16 != 0) --R;
+        if ((R * KI * s) % 16 != 0 && P.O > R) return TL_EUNSUPPORTED;
+        out = head + "\"path\": \"staged\", \"R\": " + std::to_string(R) + "}";
+    }
+    return TL_OK;
 }
 
 int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,

@@ -104,7 +104,8 @@ def ttm_case(shape, layout, mode, J, blayout, dtype, seed):
     ((5, 37, 2001), (1, 2, 3), 2, 7, (2, 1)),   # bulk-epilogue DMMA, odd J, odd tail tile
     ((3, 33, 5, 17, 2, 64), (1, 2, 3, 4, 5, 6), 2, 16, (1, 2)),  # config-5 ttm shape (smaller)
     ((9, 300, 41), (1, 2, 3), 2, 32, (1, 2)),   # J = 32, K large: B image too big -> GETT
-    ((200, 60, 3), (2, 1, 3), 1, 32, (1, 2)),   # J = 32 permuted output: staged direct stores
+    ((200, 60, 3), (2, 1, 3), 1, 32, (1, 2)),   # J = 32, B image past 48 KB: GETT, permuted output
+    ((20, 60, 3), (2, 1, 3), 1, 32, (1, 2)),    # J = 32 permuted output: staged direct stores
     # warp-specialised stream kernel edges: partial last tile with an odd
     # R*K*I (8-byte tails in and out), J in (16, 32], K < 4 and K % 4 != 0,
     # fewer tiles than SMs and than consumer warps, contracted stride 1

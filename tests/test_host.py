@@ -143,8 +143,31 @@ def test_ttm_gett_plans():
     # last-order mode 2: A's and C's fastest free dims differ -> 2-D box 8 x 16
     p = plan(1, (512,) * 3, (3, 2, 1), 2, _abi.TL_F64, (384, 512))
     assert p["sigma"][0] == [8, 1, 196608] and p["sigma"][1] == [16, 262144, 1]
-    # config 5's ttm (J = 16) is HBM-bound -> staged kernel
-    assert plan(1, (3, 33, 5, 17, 2, 640), (1, 2, 3, 4, 5, 6), 2, _abi.TL_F64, (16, 33))["path"] == "staged"
+    # config 5's ttm (J = 16) is HBM-bound -> the warp-specialised stream
+    # kernel: 8-slab tiles (24 positions = 3 whole n8 tiles), 8 consumer warps
+    # with 3 private slots each inside the 220 KB budget
+    p = plan(1, (3, 33, 5, 17, 2, 640), (1, 2, 3, 4, 5, 6), 2, _abi.TL_F64, (16, 33))
+    assert (p["path"], p["O"], p["K"], p["I"], p["J"]) == ("stream", 108800, 33, 3, 16)
+    assert (p["R"], p["NT"], p["warps"], p["slots_per_warp"]) == (8, 3, 8, 3) and p["smem"] <= 220 * 1024
+
+
+def test_ttm_small_j_plans():
+    # J = 32 on a (5, 37, 20001) tensor: tiles sized so all 8 warps keep 2 slots
+    p = plan(1, (5, 37, 20001), (1, 2, 3), 2, _abi.TL_F64, (32, 37))
+    assert p["path"] == "stream" and p["warps"] == 8 and p["slots_per_warp"] >= 2
+    assert (p["R"] * p["I"]) <= 8 * p["NT"] and p["R"] * p["K"] * p["I"] % 2 == 0
+    # no stream plan (R*I = 256 positions exceed a warp) and a bulk plan would
+    # need 512 threads for its 256-thread kernel -> the staged kernel (the
+    # wide-fuzz regression, tests/test_gpu_api.py)
+    p = plan(1, (2, 8, 16, 7, 5, 2, 8), (1, 2, 3, 4, 5, 6, 7), 4, _abi.TL_F64, (25, 7))
+    assert (p["path"], p["I"]) == ("staged", 256)
+    # permuted outputs (not in A's order) and float32/int64 go to the staged kernel
+    assert plan(1, (20, 60, 3), (2, 1, 3), 1, _abi.TL_F64, (32, 20))["path"] == "staged"
+    # a B image past 48 KB (J * K = 32 * 200) leaves the family -> GETT
+    assert plan(1, (200, 60, 3), (2, 1, 3), 1, _abi.TL_F64, (32, 200))["path"] == "gett"
+    assert plan(1, (3, 33, 5, 17), (1, 2, 3, 4), 2, _abi.TL_F32, (16, 33))["path"] == "staged"
+    # I > 256: outside the staged family -> GETT (J >= 8, GEMM-shaped) or SIMT
+    assert plan(1, (9, 31, 4), (1, 2, 3), 3, _abi.TL_F64, (15, 4))["path"] == "simt"
 
 
 def test_compute_strides_rule_and_erratum():
@@ -204,8 +227,8 @@ def test_gett_tile_store_order():
     p = plan(1, (512,) * 3, (3, 2, 1), 2, _abi.TL_F64, (384, 512))
     assert p["box"] == 64
     assert plan(1, (512,) * 3, (1, 2, 3), 2, _abi.TL_F64, (384, 512))["box"] == 0
-    # J = 32 with a small K now stays on the staged kernels
-    assert plan(1, (5, 37, 2001), (1, 2, 3), 2, _abi.TL_F64, (32, 37))["path"] == "staged"
+    # J = 32 with a small K stays on the small-J family (the stream kernel)
+    assert plan(1, (5, 37, 2001), (1, 2, 3), 2, _abi.TL_F64, (32, 37))["path"] == "stream"
 
 
 def test_product_package_never_touches_the_oracle():

@@ -247,10 +247,13 @@ struct TtvBoxParams {
     int64_t rs_as[TL_MAX_DIGITS], rs_cs[TL_MAX_DIGITS];
 };
 
-template <class TA, class TC, int VEC, int NJ, int UB = 8>
+// H warps share one chain row per pass (H = 2: a row's 2 x 32*VEC elements
+// are read as one contiguous 1 KB run for float64 instead of 512 B).
+template <class TA, class TC, int VEC, int NJ, int UB = 8, int H = 1>
 __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ TtvBoxParams P) {
     using Acc = typename AccOf<TA>::type;
-    constexpr int BA = 32 * VEC, BC = 8 * NJ, PITCH = BA + 1;
+    constexpr int RPP = 8 / H;  // chain rows per pass (one per H warps)
+    constexpr int BA = 32 * VEC * H, BC = RPP * NJ, PITCH = BA + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     if (stop_requested(P.stop)) return;
@@ -309,14 +312,14 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
             tabC[threadIdx.x] = oc;
         }
         __syncthreads();
-        const int a = lane * VEC;
+        const int a = (warp % H) * 32 * VEC + lane * VEC;
         const bool a_ok = ab * BA + a + VEC <= P.e0;
         // NJ passes of 8 chain rows (one per warp); each pass is the strided
         // kernel's k loop: U rows of VEC elements in flight per thread (U = K
         // for K = 9: one round trip per pass instead of two)
         constexpr int U = UB;
         for (int t = 0; t < NJ; ++t) {
-            const int j = warp + 8 * t;
+            const int j = warp / H + RPP * t;
             const int64_t ta = tabA[j];
             Acc acc[VEC];
 #pragma unroll
@@ -898,6 +901,7 @@ struct TtvLaunch {
     bool pdl;  // programmatic dependent launch (HOPM chains)
     bool small_cluster;  // small kernel + HOPM norm as one thread-block cluster
     bool rows_tma;     // regime S, I == 1, 2-D TMA tensor map
+    int box_h;         // regime 4: warps per chain row (1 or 2)
     CUtensorMap tmap;
     dim3 grid, block;
     size_t smem;
@@ -1066,6 +1070,10 @@ static cudaError_t launch_box(const TtvLaunch &L, cudaStream_t st) {
     // K = 9: the whole fold in flight per pass (config 5 seed 5: 150.6 ->
     // 147.2 us at the same 64 registers; K = 10..12 would need 69-78
     // registers, one CTA per SM fewer, unmeasured)
+    if (L.box_h == 2) {
+        if (L.vec == 2 && L.box.K == 9) return go(ttv_box_kernel<TA, TC, 2, 8, 9, 2>);
+        if (L.vec == 2) return go(ttv_box_kernel<TA, TC, 2, 8, 8, 2>);
+    }
     if (L.vec == 2 && L.box.K == 9) return go(ttv_box_kernel<TA, TC, 2, 8, 9>);
     if (L.vec == 2) return go(ttv_box_kernel<TA, TC, 2, 8>);
     return go(ttv_box_kernel<TA, TC, 1, 8>);
@@ -1287,7 +1295,14 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
     int vec = 1;
     if (s == 4 && d0.ext % 4 == 0 && base_addr % 16 == 0 && (cn.I % 4) == 0) vec = 4;
     else if (d0.ext % 2 == 0 && base_addr % (2 * s) == 0 && (cn.I % 2) == 0 && s <= 8) vec = 2;
-    const int64_t BA = 32 * vec, BC = 64;
+    static const int box_h_env = [] {
+        const char *e = getenv("TL_TTV_BOX_H");
+        return e ? atoi(e) : 2;
+    }();
+    // two warps per chain row (1 KB runs along d0) for float64 pairs when d0 is long enough
+    const int h = (box_h_env == 2 && vec == 2 && s == 8 && d0.ext >= 128) ? 2 : 1;
+    L.box_h = h;
+    const int64_t BA = 32 * vec * h, BC = 64 / h;
     B.nA = (d0.ext + BA - 1) / BA;
     B.nJ = (cext + BC - 1) / BC;
     B.nrest = nrest;

@@ -998,8 +998,17 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
         if (P.I % 2 == 0 && base_addr % 16 == 0) vec = 2;
     }
     const int64_t nthreads = P.O * (P.I / vec);
+    static const int slab_align = [] {
+        const char *e = getenv("TL_TTV_SLAB_CTA");
+        return e ? atoi(e) : 1;
+    }();
     int threads = 256;
     while (threads > 32 && (nthreads + threads - 1) / threads < 2 * nsm) threads /= 2;
+    // one o-slab per CTA when a slab's fibers fill 128..256 threads (HOPM's
+    // 400^3 mode-2 pass: 200): a slab's warps then advance through k together
+    // and read each k-row as one contiguous run
+    const int64_t per_slab = P.I / vec;
+    if (slab_align && P.O > 1 && per_slab >= 128 && per_slab <= 256 && (P.O >= 2 * nsm)) threads = (int)per_slab;
     P.b_smem = (P.K <= 8192) ? 1 : 0;
     P.in_vec_ok = (P.in_map.n >= 1 && P.in_map.div[0].d % (uint32_t)vec == 0) ? 1 : 0;
     static const int64_t omul_env = [] {

@@ -450,8 +450,9 @@ __global__ void __launch_bounds__(256) ttm_bulk_kernel(const __grid_constant__ T
 // HBM-bound stream of short tiles (config 5: 6 KB per tile).
 // Private rings keep every barrier wait unambiguous: a slot's successive
 // phases are waited on by one warp (and by the producer) strictly in order,
-// so no waiter ever asks for a phase two ahead of the barrier (an mbarrier
-// parity wait cannot tell phase n+2 from phase n).
+// so nobody waits for phase n+1 while phase n is still open -- a parity wait
+// for n+1 would return at once then (it reads as the completed phase n-1).
+// A shared round-robin ring allowed exactly that and hung at J = 32.
 // Same per-element arithmetic as the other DMMA kernels (k-ordered FMA).
 constexpr int kStreamMaxSlots = 48;
 constexpr size_t kStreamSmemBudget = 220 * 1024;  // one CTA per SM (227 KB max)

@@ -68,6 +68,11 @@ int32_t tl_device_arch(void);
 /* Thread-local description of the last error (never NULL). */
 const char *tl_last_error(void);
 
+/* Optional: initialise the library's CUDA runtime state on the current
+ * device and load its small kernels (a process's first call otherwise pays
+ * the lazy-loading cost, ~3-12 ms).  No reference counterpart. */
+int tl_init(void);
+
 /* ttv -- contraction.py:113-131 (ttv(a, b, mode)).
  * C(i_1..i_{m-1}, i_{m+1}..i_p) = sum_k A(..k..) * b(k), k sequential.
  * b: order-1 of length n_mode, or an (n_mode, 1) column.  c: dense
@@ -95,6 +100,14 @@ size_t tl_reduce_workspace_bytes(void);
  * result_dev: device double (floats) or int64 (int64 operands). */
 int tl_inner(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr,
              void *result_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* inner_product_flat(a, b, init) -- elementwise.py:411-414: as tl_inner,
+ * with the fold starting at *init (a HOST scalar of the result type:
+ * double for floating operands, int64 for int64 operands; NULL = 0).  init
+ * enters the compensated sum before its single final rounding, as the
+ * reference's `acc = init; acc += a*b` starts from it. */
+int tl_inner_flat(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr,
+                  const void *init, void *result_dev, void *ws, size_t ws_bytes, void *stream);
 
 /* frobenius_norm -- contraction.py:462-464: *result_dev = sqrt(<a, a>). */
 int tl_frobenius_norm(const tl_desc *a, const void *a_ptr, double *result_dev,

@@ -23,6 +23,7 @@ from .contraction import (
     ttt,
     ttv,
 )
+from .iterators import MultiIterator, StrideIterator, fill_range, inner_product_range, walk_positions
 from .hopm import DegenerateInputError, HopmRunner, HopmState, hopm, rank_one_compose, residual
 from .layout import (
     MAX_INDEX,
@@ -41,6 +42,11 @@ from .views import Range, TensorView, classify_view
 __version__ = "0.1.0"
 
 __all__ = [
+    "MultiIterator",
+    "StrideIterator",
+    "fill_range",
+    "inner_product_range",
+    "walk_positions",
     "Range",
     "TensorView",
     "classify_view",

@@ -26,10 +26,12 @@ EXPORTS = (
     "tl_abi_version",
     "tl_device_arch",
     "tl_last_error",
+    "tl_init",
     "tl_ttv",
     "tl_ttm",
     "tl_reduce_workspace_bytes",
     "tl_inner",
+    "tl_inner_flat",
     "tl_frobenius_norm",
     "tl_hopm_workspace_bytes",
     "tl_hopm",
@@ -86,10 +88,12 @@ def load_library(path: str = LIB_PATH):
         L.tl_abi_version.restype = ctypes.c_int32
         L.tl_device_arch.restype = ctypes.c_int32
         L.tl_last_error.restype = ctypes.c_char_p
+        L.tl_init.restype = ctypes.c_int
         L.tl_ttv.argtypes = [_dp, _vp, _dp, _vp, _dp, _vp, ctypes.c_int32, _vp]
         L.tl_ttm.argtypes = [_dp, _vp, _dp, _vp, _dp, _vp, ctypes.c_int32, _vp]
         L.tl_reduce_workspace_bytes.restype = ctypes.c_size_t
         L.tl_inner.argtypes = [_dp, _vp, _dp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+        L.tl_inner_flat.argtypes = [_dp, _vp, _dp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_frobenius_norm.argtypes = [_dp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_hopm_workspace_bytes.argtypes = [_dp, ctypes.POINTER(ctypes.c_size_t)]
         vpp = ctypes.POINTER(_vp)
@@ -103,7 +107,7 @@ def load_library(path: str = LIB_PATH):
         L.tl_rank_one_compose.argtypes = [_dp, vpp, _vp, _vp, _vp]
         L.tl_residual.argtypes = [_dp, _vp, vpp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_plan_describe.argtypes = [ctypes.c_int32, _dp, _dp, ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
-        for name in ("tl_ttv", "tl_ttm", "tl_inner", "tl_frobenius_norm", "tl_hopm_workspace_bytes", "tl_hopm",
+        for name in ("tl_ttv", "tl_ttm", "tl_inner", "tl_inner_flat", "tl_frobenius_norm", "tl_hopm_workspace_bytes", "tl_hopm",
                      "tl_hopm_graph_create", "tl_graph_launch", "tl_graph_destroy", "tl_copy", "tl_rank_one_compose",
                      "tl_residual", "tl_plan_describe"):
             getattr(L, name).restype = ctypes.c_int
@@ -116,6 +120,24 @@ def lib():
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1711_10912_b200 needs a CUDA (sm_100a) device; there is no CPU fallback")
     return load_library()
+
+
+_warm_devices = set()
+
+
+def warm(device) -> None:
+    """Once per device: tl_init (the library's runtime state and its small
+    kernels), so the first hot-path call of a process is not ms-slow.  Runs
+    when the first DenseTensor is placed on ``device``."""
+    if device.type != "cuda":
+        raise RuntimeError(f"paper_1711_10912_b200 tensors live on a CUDA device, not {device}; there is no CPU fallback")
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx in _warm_devices:
+        return
+    L = lib()
+    with torch.cuda.device(idx):
+        check(L.tl_init(), "init")
+    _warm_devices.add(idx)
 
 
 def check(rc: int, what: str = "") -> None:

@@ -11,7 +11,9 @@ Every numeric step runs in hand-written sm_100a kernels behind the C ABI
 
 from __future__ import annotations
 
+import ctypes
 import math
+import numbers
 from dataclasses import dataclass
 from typing import Sequence, Tuple
 
@@ -117,16 +119,23 @@ def _reduce_result_buffer(dtype, device) -> torch.Tensor:
     return torch.empty(1, dtype=torch.int64 if dtype == torch.int64 else torch.float64, device=device)
 
 
-def inner_product_device(a, b) -> torch.Tensor:
-    """sum_i a[i] b[i] as a 1-element device tensor (no host sync)."""
+def inner_product_device(a, b, init=None) -> torch.Tensor:
+    """init + sum_i a[i] b[i] as a 1-element device tensor (no host sync).
+    ``init`` (a host scalar, default 0) is the fold's starting value; for
+    floating operands it enters the compensated sum before the single final
+    rounding, for int64 operands it must be an integer."""
     A, B = _operand(a), _operand(b)
     if A.shape != B.shape:
         raise ValueError(f"shape mismatch: {B.shape} vs {A.shape}")
     res = _reduce_result_buffer(A.dtype, A.device)
     ws = _abi.reduce_workspace(A.device)
     L = _abi.lib()
-    rc = L.tl_inner(A.desc(), A.ptr(), B.desc(), B.ptr(), res.data_ptr(), ws.data_ptr(), ws.numel(),
-                    _abi.stream_handle())
+    init_ref = None
+    if init is not None:
+        init_ref = ctypes.c_int64(int(init)) if A.dtype == torch.int64 else ctypes.c_double(float(init))
+    rc = L.tl_inner_flat(A.desc(), A.ptr(), B.desc(), B.ptr(),
+                         ctypes.byref(init_ref) if init_ref is not None else None, res.data_ptr(),
+                         ws.data_ptr(), ws.numel(), _abi.stream_handle())
     _abi.check(rc, "inner")
     return res
 
@@ -137,8 +146,16 @@ def inner_product_tensors(a, b):
 
 
 def inner_product_flat(a, b, init=0):
-    """init + sum_i a[i] * b[i] (elementwise.py:411-414)."""
-    return init + inner_product_tensors(a, b)
+    """init + sum_i a[i] * b[i] by multi-index (elementwise.py:411-433).
+
+    The reference folds ``acc = init; acc += a[i]*b[i]``: the device sum
+    starts from ``init`` too (it is not added to a rounded total).  An
+    integer operand pair with a non-integral ``init`` sums exactly and adds
+    ``init`` once on the host, as Python's int + float would."""
+    A = _operand(a)
+    if A.dtype == torch.int64 and not isinstance(init, numbers.Integral):
+        return init + inner_product_tensors(a, b)
+    return inner_product_device(a, b, init).item()
 
 
 def frobenius_norm_device(a) -> torch.Tensor:
@@ -252,10 +269,13 @@ class ContractionSpec:
 
 
 def _relayouted(T: DenseTensor, layout) -> DenseTensor:
-    """A copy of T stored under ``layout`` (device tl_copy)."""
+    """A copy of T stored under ``layout`` (device tl_copy); internal
+    scratch, so not a counted DenseTensor allocation (the reference's ttt
+    allocates only its output, test_contraction.py:398-425)."""
     if tuple(layout) == T.layout:
         return T
-    out = DenseTensor(T.shape, layout=tuple(layout), dtype=T.dtype, device=T.device, fill_value=None)
+    meta = TensorMeta(T.shape, layout=tuple(layout))
+    out = DenseTensor._wrap(meta, torch.empty(T.size, dtype=T.dtype, device=T.device))
     _copy(T.desc(), T.buffer, out.desc(), out.buffer)
     return out
 
@@ -298,7 +318,9 @@ def ttt(a, b, spec: ContractionSpec) -> DenseTensor:
         ws = _abi.reduce_workspace(A.device)
         _abi.check(L.tl_inner(view(A, phi), A.ptr(), view(B, psi), B.ptr(), res.data_ptr(), ws.data_ptr(),
                               ws.numel(), _abi.stream_handle()), "ttt")
-        return DenseTensor._wrap(TensorMeta((1,)), res.to(A.dtype))
+        out = DenseTensor((1,), dtype=A.dtype, device=A.device, fill_value=None)
+        out.buffer.copy_(res)
+        return out
     if q == 1 and (s == 0 or r == 0):
         # one operand is a vector: ttv over a permuted view, the reference's
         # fold bit for bit (x*y commutes)

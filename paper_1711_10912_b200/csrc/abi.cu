@@ -29,11 +29,12 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
                        int m0, cudaStream_t st);
 size_t reduce_workspace_bytes();
 int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const void *b_ptr, void *result,
-                   bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st);
+                   bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st, const void *init = nullptr);
 int hopm_workspace(const tl_desc &a, size_t *bytes);
 int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, double *const *u, int32_t max_sweeps,
                  double tol, double *l, double *hist, int32_t *info, double *resid, void *ws, size_t ws_bytes,
                  cudaStream_t st);
+void copy_preload();
 int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_ptr, cudaStream_t st);
 int rank_one_enqueue(const tl_desc &shape, const double *const *u, const double *scale_dev, double *out,
                      cudaStream_t st);
@@ -142,6 +143,16 @@ int32_t tl_device_arch(void) {
 }
 
 const char *tl_last_error(void) { return g_error.c_str(); }
+
+int tl_init(void) {
+    // the library's runtime state, the current device's attributes and the
+    // small-copy kernels, so a process's first hot-path call is not ms-slow
+    cudaError_t e = cudaFree(nullptr);
+    if (e != cudaSuccess) return cuda_status(e, "init");
+    (void)device_info();
+    copy_preload();
+    return cuda_status(cudaGetLastError(), "init");
+}
 
 int tl_ttv(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr, const tl_desc *c, void *c_ptr,
            int32_t mode, void *stream) {
@@ -254,15 +265,20 @@ static bool same_shape(const tl_desc &a, const tl_desc &b) {
     return true;
 }
 
-int tl_inner(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr, void *result_dev, void *ws,
-             size_t ws_bytes, void *stream) {
+int tl_inner_flat(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr, const void *init,
+                  void *result_dev, void *ws, size_t ws_bytes, void *stream) {
     if (!check_desc(a, "inner A") || !check_desc(b, "inner B")) return TL_EINVAL;
     if (!same_shape(*a, *b)) {
         set_error("shape mismatch");
         return TL_EINVAL;
     }
     if (!check_ptrs("inner", {a_ptr, b_ptr, result_dev, ws})) return TL_EINVAL;
-    return reduce_enqueue(*a, a_ptr, *b, b_ptr, result_dev, false, ws, ws_bytes, (cudaStream_t)stream);
+    return reduce_enqueue(*a, a_ptr, *b, b_ptr, result_dev, false, ws, ws_bytes, (cudaStream_t)stream, init);
+}
+
+int tl_inner(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_ptr, void *result_dev, void *ws,
+             size_t ws_bytes, void *stream) {
+    return tl_inner_flat(a, a_ptr, b, b_ptr, nullptr, result_dev, ws, ws_bytes, stream);
 }
 
 int tl_frobenius_norm(const tl_desc *a, const void *a_ptr, double *result_dev, void *ws, size_t ws_bytes,

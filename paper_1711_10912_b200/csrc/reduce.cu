@@ -96,6 +96,8 @@ struct ReduceParams {
     double *partials;
     unsigned int *ticket;
     int32_t sqrt_result;
+    double init_f;    // inner_product_flat's init (elementwise.py:411): the fold's starting value
+    int64_t init_i;
     int64_t n_rows, row_len;  // dot_rows
     DigitMap rows_a, rows_b;  // row index -> element offsets
     // dot_tiled
@@ -139,12 +141,13 @@ __device__ __forceinline__ Acc64 load_partial(const double *partials, int idx, A
     return Acc64{(int64_t)__ldcg((const long long *)partials + 2 * idx)};
 }
 __device__ __forceinline__ void write_result(const ReduceParams &P, DD v) {
+    two_sum_add(v, P.init_f);  // init enters the compensated sum before its single final rounding
     double r = v.hi + v.lo;
     if (P.sqrt_result) r = sqrt(r);
     *(double *)P.result = r;
 }
 __device__ __forceinline__ void write_result(const ReduceParams &P, Acc64 v) {
-    *(int64_t *)P.result = v.v;
+    *(int64_t *)P.result = (int64_t)((uint64_t)v.v + (uint64_t)P.init_i);
 }
 
 // Per-CTA partial -> global; last CTA folds partials in index order.
@@ -547,7 +550,7 @@ int residual_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u
 size_t reduce_workspace_bytes() { return (size_t)kMaxPartials * 2 * sizeof(double) + 256; }
 
 int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const void *b_ptr, void *result,
-                   bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st) {
+                   bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st, const void *init) {
     if (ws == nullptr || ws_bytes < reduce_workspace_bytes()) {
         set_error("inner/norm: workspace of %zu bytes required", reduce_workspace_bytes());
         return TL_EWORKSPACE;
@@ -566,6 +569,10 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
     P.partials = (double *)ws;
     P.ticket = (unsigned int *)((unsigned char *)ws + (size_t)kMaxPartials * 2 * sizeof(double));
     P.sqrt_result = do_sqrt ? 1 : 0;
+    if (init != nullptr) {
+        if (a.dtype == TL_I64) P.init_i = *(const int64_t *)init;
+        else P.init_f = *(const double *)init;
+    }
     const int64_t N = volume(a);
     const bool same_fast = da.empty() || db.empty() || da[0] == db[0];
     const bool is_int = a.dtype == TL_I64;

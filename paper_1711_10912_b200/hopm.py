@@ -80,6 +80,20 @@ def _start_vectors(shape, u0) -> List[List[float]]:
     return out
 
 
+_EXACT_INT = 1 << 53
+
+
+def _floating(a: DenseTensor) -> DenseTensor:
+    """int64 tensors enter HOPM as float64: the reference multiplies its
+    Python ints by float vector entries, i.e. converts each to binary64
+    first, which is exact below 2^53 (checked; larger values raise)."""
+    if a.dtype in (torch.float32, torch.float64):
+        return a
+    if a.size and int(a.buffer.abs().max().item()) > _EXACT_INT:
+        raise NotImplementedError("hopm: int64 entries beyond 2^53 are not exactly representable in binary64")
+    return a.to(torch.float64)
+
+
 def _vec(t: torch.Tensor) -> DenseTensor:
     return DenseTensor._wrap(TensorMeta((t.numel(),)), t)
 
@@ -92,9 +106,7 @@ class HopmRunner:
                  track_residuals: bool = False):
         if max_sweeps < 1:
             raise ValueError("max_sweeps must be >= 1")
-        a = as_dense_operand(a)
-        if a.dtype not in (torch.float32, torch.float64):
-            raise NotImplementedError("hopm requires floating elements")
+        a = _floating(as_dense_operand(a))
         self.a = a
         self.max_sweeps = int(max_sweeps)
         self.tol = float(tol)
@@ -192,7 +204,7 @@ def rank_one_compose(scale: float, vectors: Sequence) -> DenseTensor:
 
 def residual(a, state: HopmState) -> float:
     """||a - rank_one_compose(state.scale, state.u)||_F (hopm.py:142-147)."""
-    a = as_dense_operand(a)
+    a = _floating(as_dense_operand(a))
     vs, ptrs = _vector_ptrs(state.u, a.device)
     sc = torch.tensor([float(state.l[-1])], dtype=torch.float64, device=a.device)
     res = torch.empty(1, dtype=torch.float64, device=a.device)

@@ -9,8 +9,10 @@ differs, by design:
 * the element type is explicit: ``dtype`` in {float64 (default), float32,
   int64}.  ``from_memory`` infers it (all-int -> int64, else float64,
   float32 only when the source is float32);
-* ``.data`` is a host round trip (download on get, upload on set) kept for
-  compatibility with code that reads/assigns the reference's list;
+* ``.data`` is a host snapshot list in memory-index order whose element and
+  slice writes go through to the device buffer (``t.data[j] = v`` works as
+  on the reference's storage list, hopm.py:138, views.py:222); operations
+  that would change the length raise, since the storage size is fixed;
 * relayout/assign run on the device (tl_copy).
 """
 
@@ -22,6 +24,7 @@ import numpy as np
 import torch
 
 from . import _abi
+from .iterators import MultiIterator, StrideIterator
 from .layout import TensorMeta, memory_index, validate_layout, validate_shape, volume
 
 __all__ = ["DenseTensor", "tensors_equal", "as_dtype"]
@@ -54,6 +57,75 @@ def _default_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def _device(device) -> torch.device:
+    dev = torch.device(device) if device is not None else _default_device()
+    _abi.warm(dev)
+    return dev
+
+
+def _checked_scalar(dtype: torch.dtype, value):
+    """A value about to be stored into an element of ``dtype``.  Integer
+    storage refuses values it cannot hold exactly (the reference's list
+    would keep them; torch would truncate silently)."""
+    if dtype == torch.int64 and not isinstance(value, numbers.Integral):
+        f = float(value)
+        if not f.is_integer():
+            raise TypeError(f"cannot store {value!r} in an int64 tensor exactly; convert it with .to('float64')")
+        return int(f)
+    return value
+
+
+class _DataList(list):
+    """Snapshot of a device buffer in memory-index order whose writes go
+    through to the buffer (the reference's ``.data`` *is* the storage list,
+    tensor.py:46).  Reads are the values at the time ``.data`` was taken;
+    every element or same-length slice write updates both this list and
+    the device buffer.  Length-changing operations raise TypeError."""
+
+    __slots__ = ("_buf",)
+
+    def __init__(self, buf: torch.Tensor):
+        super().__init__(buf.cpu().tolist())
+        self._buf = buf
+
+    def __setitem__(self, key, value):
+        n = len(self)
+        if isinstance(key, slice):
+            idx = range(n)[key]
+            vals = list(value)
+            if len(vals) != len(idx):
+                raise TypeError("tensor storage has a fixed size: slice assignment must keep the length")
+            vals = [_checked_scalar(self._buf.dtype, v) for v in vals]
+            list.__setitem__(self, key, vals)
+            if vals:
+                pos = torch.as_tensor(list(idx), dtype=torch.int64).to(self._buf.device)
+                self._buf[pos] = torch.as_tensor(vals, dtype=self._buf.dtype).to(self._buf.device)
+            return
+        j = key.__index__()
+        if not -n <= j < n:
+            raise IndexError("list assignment index out of range")
+        j %= n
+        v = _checked_scalar(self._buf.dtype, value)
+        list.__setitem__(self, j, v)
+        self._buf[j] = v
+
+    def _fixed(self, *args, **kwargs):
+        raise TypeError("tensor storage has a fixed size; assign whole-list data through the .data setter")
+
+    append = extend = insert = pop = remove = clear = __delitem__ = __iadd__ = __imul__ = _fixed
+
+    def _write_all(self):
+        self._buf.copy_(torch.as_tensor(list(self), dtype=self._buf.dtype))
+
+    def sort(self, *args, **kwargs):
+        list.sort(self, *args, **kwargs)
+        self._write_all()
+
+    def reverse(self):
+        list.reverse(self)
+        self._write_all()
+
+
 def _infer_dtype(data) -> torch.dtype:
     if isinstance(data, torch.Tensor):
         if data.dtype in (torch.float32, torch.float64, torch.int64):
@@ -83,7 +155,7 @@ class DenseTensor:
         outputs, which the kernels overwrite completely)."""
         self.meta = TensorMeta(shape, offsets, layout)
         dt = as_dtype(dtype)
-        dev = torch.device(device) if device is not None else _default_device()
+        dev = _device(device)
         if fill_value is None:
             self.buffer = torch.empty((self.meta.size,), dtype=dt, device=dev)
         else:
@@ -105,7 +177,7 @@ class DenseTensor:
         or device; a pinned host tensor is copied asynchronously)."""
         meta = TensorMeta(shape, offsets, layout)
         dt = as_dtype(dtype) if dtype is not None else _infer_dtype(data)
-        dev = torch.device(device) if device is not None else _default_device()
+        dev = _device(device)
         if isinstance(data, torch.Tensor):
             src = data.reshape(-1)
             buf = torch.empty(src.numel(), dtype=dt, device=dev)
@@ -161,16 +233,24 @@ class DenseTensor:
     # -- host interchange ------------------------------------------------------------
     @property
     def data(self) -> list:
-        """Host copy of the buffer in memory-index order (a round trip)."""
-        return self.buffer.cpu().tolist()
+        """The buffer in memory-index order as a host list whose element and
+        slice writes go through to the device (see ``_DataList``)."""
+        return _DataList(self.buffer)
 
     @data.setter
     def data(self, values) -> None:
-        src = values if isinstance(values, torch.Tensor) else torch.as_tensor(
-            np.asarray(list(values) if not isinstance(values, np.ndarray) else values))
-        src = src.reshape(-1)
+        """Replace every element (memory-index order).  An int64 tensor that
+        is given non-integral values becomes float64, as the reference's
+        list would simply hold them."""
+        if isinstance(values, torch.Tensor):
+            src = values.reshape(-1)
+        else:
+            arr = values if isinstance(values, np.ndarray) else np.asarray(list(values))
+            src = torch.as_tensor(np.ascontiguousarray(arr.reshape(-1)))
         if src.numel() != self.meta.size:
             raise ValueError(f"data length {src.numel()} does not match volume {self.meta.size}")
+        if self.dtype == torch.int64 and src.is_floating_point() and not bool(torch.all(src == torch.round(src))):
+            self.buffer = torch.empty(self.meta.size, dtype=torch.float64, device=self.device)
         self.buffer.copy_(src.to(self.dtype))
 
     def numpy(self) -> np.ndarray:
@@ -193,7 +273,7 @@ class DenseTensor:
         return self.buffer[memory_index(self.strides, self._key(key), self.offsets)].item()
 
     def __setitem__(self, key, value):
-        self.buffer[memory_index(self.strides, self._key(key), self.offsets)] = value
+        self.buffer[memory_index(self.strides, self._key(key), self.offsets)] = _checked_scalar(self.dtype, value)
 
     def get_memory(self, j: int):
         if not 0 <= j < self.size:
@@ -203,7 +283,7 @@ class DenseTensor:
     def set_memory(self, j: int, value) -> None:
         if not 0 <= j < self.size:
             raise IndexError(f"memory index {j} out of range [0, {self.size})")
-        self.buffer[j] = value
+        self.buffer[j] = _checked_scalar(self.dtype, value)
 
     def item(self):
         if self.size != 1:
@@ -249,10 +329,43 @@ class DenseTensor:
     def to(self, dtype) -> "DenseTensor":
         return DenseTensor._wrap(self.meta, self.buffer.to(as_dtype(dtype)))
 
+    # -- iterators (tensor.py:204-235) ----------------------------------------------------
+    def miter(self) -> MultiIterator:
+        """Cursor at the first element over the device buffer; accepted by
+        every hot-path function as an operand (contraction.py:52-55)."""
+        return MultiIterator(self.buffer, 0, self.strides, self.shape)
+
+    def dim_begin(self, dim: int, at=None) -> StrideIterator:
+        """Stride iterator over dimension ``dim`` (one-based); ``at`` fixes
+        the other coordinates as an absolute multi-index."""
+        return StrideIterator(self.buffer, self._dim_base(dim, at), self.strides[dim - 1])
+
+    def dim_end(self, dim: int, at=None) -> StrideIterator:
+        w = self.strides[dim - 1]
+        return StrideIterator(self.buffer, self._dim_base(dim, at) + self.shape[dim - 1] * w, w)
+
+    def _dim_base(self, dim: int, at) -> int:
+        if not 1 <= dim <= self.order:
+            raise ValueError(f"dimension {dim} out of range 1..{self.order}")
+        if at is None:
+            return 0
+        if len(at) != self.order:
+            raise ValueError(f"expected {self.order} indices, got {len(at)}")
+        return sum(self.strides[r] * (at[r] - self.offsets[r]) for r in range(self.order) if r != dim - 1)
+
+    def view(self, *ranges):
+        """Rectangular view (tensor.py:237-250): one range per dimension, or
+        one sequence of them."""
+        from .views import TensorView
+
+        if len(ranges) == 1 and isinstance(ranges[0], (list, tuple)):
+            ranges = tuple(ranges[0])
+        return TensorView(self, ranges)
+
     # -- interchange -------------------------------------------------------------------
     def to_dict(self) -> dict:
         return {"shape": list(self.shape), "layout": list(self.layout), "offsets": list(self.offsets),
-                "data": self.data}
+                "data": self.buffer.cpu().tolist()}
 
     @classmethod
     def from_dict(cls, obj: dict) -> "DenseTensor":

@@ -49,6 +49,14 @@ NORM_BYTES = 4 * N4
 INNER_BYTES = 8 * N4
 STEP_BYTES = 12 * TTV_BYTES + NORM_BYTES + INNER_BYTES
 FP64_PEAK_TFLOPS = 37.0  # DMMA/DFMA, measured by tools/fp64_probe.cu (profiles/fp64_probe_r01.txt)
+L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2: written between cold-timed launches
+
+
+def cfg2_config(world):
+    """The workload's config object -- identical for both arms."""
+    return {"workload": "cfg2: ttv q=1..4 x {first,last,perm(3,1,2,4)} + inner + norm, f32 128^4 (1 GiB)",
+            "step_bytes": STEP_BYTES, "l2": "inputs 1 GiB each > 126 MB L2 (no flush needed)",
+            "parallelism": f"{world} independent replicas (weak scaling, no collective)"}
 
 
 def measured_peaks():
@@ -245,50 +253,106 @@ def time_device(fn, steps, warmup, world=1):
     return t0.elapsed_time(t1) / steps
 
 
-def e2e_step(wl):
-    """Public API end to end: the abstract tensor T (first-order) and T2 are
-    uploaded from pinned host memory, the last-order and permuted copies of
-    T are produced on the device with DenseTensor.relayout, the 14 ops run,
-    and every ttv output plus both scalars are read back to the host.  T2's
-    upload overlaps the ttvs (second stream)."""
+def e2e_step(wl, relayout_on_device=False):
+    """Public API end to end, every step from pinned host memory.
+
+    Default (the reference arm's input contract, three host buffers per
+    step): the first-order, last-order and permuted buffers of T and the
+    first-order T2 are uploaded (copy stream; each layout's four ttvs start
+    as soon as its buffer has landed), the 14 ops run, and every ttv
+    output plus both scalars are read back to the host (a third stream, so
+    downloads overlap uploads on the other copy engine).
+
+    ``relayout_on_device``: only T and T2 are uploaded; the last-order and
+    permuted copies are made on the device with DenseTensor.relayout."""
     import torch
 
     tl = wl.tl
     h2d = d2h = 0
-    pinned_T, first = wl.pinned["first"]
-    A = {"first": tl.DenseTensor.from_memory(W.CFG2_SHAPE, pinned_T, layout=first)}
-    h2d += pinned_T.numel() * 4
+    cur = torch.cuda.current_stream()
+    up, down = wl.up_stream, wl.down_stream
+    up.wait_stream(cur)
     vecs = [tl.DenseTensor.from_memory((128,), v) for v in wl.pinned_vecs]
     h2d += 4 * 128 * 4
-    side = wl.side_stream
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
+    A, ready = {}, {}
+    names = ["first"] if relayout_on_device else list(W.CFG2_LAYOUTS)
+    with torch.cuda.stream(up):
+        for name in names:
+            buf, layout = wl.pinned[name]
+            A[name] = tl.DenseTensor.from_memory(W.CFG2_SHAPE, buf, layout=layout)
+            h2d += buf.numel() * 4
+            ready[name] = torch.cuda.Event()
+            ready[name].record(up)
         B = tl.DenseTensor.from_memory(W.CFG2_SHAPE, wl.pinned_T2, layout=(1, 2, 3, 4))
-    h2d += wl.pinned_T2.numel() * 4
-    for name, layout in W.CFG2_LAYOUTS.items():
-        if name != "first":
-            t = A["first"].copy()
-            t.relayout(layout)
-            A[name] = t
+        h2d += wl.pinned_T2.numel() * 4
+        ready["T2"] = torch.cuda.Event()
+        ready["T2"].record(up)
+    for t in list(A.values()) + [B]:
+        t.buffer.record_stream(cur)
+    cur.wait_event(ready["first"])
+    if relayout_on_device:
+        for name, layout in W.CFG2_LAYOUTS.items():
+            if name != "first":
+                t = A["first"].copy()
+                t.relayout(layout)
+                A[name] = t
     res = []
     for name in W.CFG2_LAYOUTS:
+        if name in ready:
+            cur.wait_event(ready[name])
         for mode in (1, 2, 3, 4):
             c = tl.ttv(A[name], vecs[mode - 1], mode)
-            host = torch.empty(c.size, dtype=c.dtype, pin_memory=True)
-            host.copy_(c.buffer, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cur)
+            down.wait_event(done)
+            with torch.cuda.stream(down):
+                host = torch.empty(c.size, dtype=c.dtype, pin_memory=True)
+                host.copy_(c.buffer, non_blocking=True)
+            c.buffer.record_stream(down)
             res.append(host)
             d2h += c.size * 4
-    nrm = tl.frobenius_norm(A["first"])
-    torch.cuda.current_stream().wait_stream(side)
-    B.buffer.record_stream(torch.cuda.current_stream())
-    ip = tl.inner_product_tensors(A["first"], B)
+    nrm = C_norm(A["first"])
+    cur.wait_event(ready["T2"])
+    ip = C_inner(A["first"], B)
+    scal = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    scal[0:1].copy_(nrm, non_blocking=True)
+    scal[1:2].copy_(ip, non_blocking=True)
     d2h += 16
     torch.cuda.synchronize()
-    return h2d, d2h, (res, nrm, ip)
+    return h2d, d2h, (res, scal)
+
+
+def C_norm(a):
+    import paper_1711_10912_b200.contraction as C
+
+    return C.frobenius_norm_device(a)
+
+
+def C_inner(a, b):
+    import paper_1711_10912_b200.contraction as C
+
+    return C.inner_product_device(a, b)
+
+
+def time_e2e(wl, steps, warmup, world, relayout_on_device=False):
+    import torch
+
+    for _ in range(warmup):  # also warms the pinned host-buffer cache
+        e2e_step(wl, relayout_on_device)
+    barrier(world)
+    torch.cuda.synchronize()
+    te = time.perf_counter()
+    n = max(1, min(5, steps))
+    for _ in range(n):
+        h2d, d2h, res = e2e_step(wl, relayout_on_device)
+        del res
+    dt = dist_max((time.perf_counter() - te) / n, world)
+    return {"value": round(world * STEP_BYTES / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 2)}
 
 
 # ------------------------------------------------------------------ components
-def components(args):
+def components(args, wl=None):
     """Per-config numbers on rank 0 (each a median of CUDA-event timings)."""
     import torch
 
@@ -324,6 +388,26 @@ def components(args):
         del g
         return statistics.median(ts)
 
+    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def cold(fn, iters=7, warm=2):
+        """Median device time of one launch with a cold L2: a 512 MB write
+        (4x L2) runs before each timed launch, outside its events (the host
+        enqueues the launch while the flush runs, so no launch gap)."""
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            flush_buf.fill_(float(len(ts)))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
     def med_eager(fn, iters=5, warm=2):
         for _ in range(warm):
             fn()
@@ -339,6 +423,20 @@ def components(args):
         return statistics.median(ts)
 
     peak, _ = hbm_peak()
+    # config 2 extras: the first x last mixed-layout inner product (SURVEY
+    # a6) and the layout conversions the e2e relies on (relayout/transpose)
+    if wl is not None:
+        Af, Al = wl.A["first"], wl.A["last"]
+        ms = med_eager(lambda: C.inner_product_device(Af, Al), iters=7)
+        out["cfg2_inner_first_x_last_us"] = round(ms * 1e3, 1)
+        out["cfg2_inner_first_x_last_frac_hbm"] = round(INNER_BYTES / (ms * 1e-3) / 1e9 / peak, 3)
+        relay = {}
+        for name, tau in (("first_to_last", (4, 3, 2, 1)), ("first_to_perm3124", (3, 1, 2, 4)),
+                          ("first_to_2134", (2, 1, 3, 4))):
+            ms = med_eager(lambda: tl.transpose(Af, tau), iters=7)
+            relay[name] = {"us": round(ms * 1e3, 1), "frac_hbm": round(2 * 4 * N4 / (ms * 1e-3) / 1e9 / peak, 3)}
+        out["cfg2_transpose"] = relay
+        torch.cuda.empty_cache()
     # config 1
     T, b = W.cfg1()
     A = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, (1, 2, 3)))
@@ -389,26 +487,32 @@ def components(args):
         Bm5 = tl.DenseTensor.from_memory(M.shape, W.layout_buffer(M, (1, 2)))
         t_ttv = med(lambda: tl.ttv(A, Vv, 5))
         C1 = tl.ttv(A, Vv, 5)
-        t_ttm = med(lambda: tl.ttm(C1, Bm5, 2))
+        t_ttm = cold(lambda: tl.ttm(C1, Bm5, 2))
+        t_ttm_warm = med(lambda: tl.ttm(C1, Bm5, 2))
         C2 = tl.ttm(C1, Bm5, 2)
-        t_nrm = med(lambda: C.frobenius_norm_device(C2))
+        t_nrm = cold(lambda: C.frobenius_norm_device(C2))
+        t_nrm_warm = med(lambda: C.frobenius_norm_device(C2))
 
         def chain():
             c1 = tl.ttv(A, Vv, 5)
             return C.frobenius_norm_device(tl.ttm(c1, Bm5, 2))
 
         # the whole config as the reference states it: ttv -> ttm -> norm of
-        # the result (intermediates L2-resident where they fit, as in any run)
-        t_chain = med(chain, reps=5)
+        # the result, from a cold L2 (the intermediates then stay L2-resident
+        # where they fit, as in any run)
+        t_chain = cold(chain)
         n5 = 96940800
         chain_bytes = 8 * (n5 + 9 + n5 // 9) + 8 * (10771200 + 528 + 5222400) + 8 * 5222400
         out[f"cfg5_seed{seed}"] = {
             "layout": list(layout),
             "ttv_us": round(t_ttv * 1e3, 1), "ttv_frac_hbm": round(8 * (n5 + 9 + n5 // 9) / (t_ttv * 1e-3) / 1e9 / peak, 3),
-            "ttm_us": round(t_ttm * 1e3, 1),
-            "ttm_frac_hbm": round(8 * (10771200 + 528 + 5222400) / (t_ttm * 1e-3) / 1e9 / peak, 3),
-            "norm_us": round(t_nrm * 1e3, 1), "norm_frac_hbm": round(8 * 5222400 / (t_nrm * 1e-3) / 1e9 / peak, 3),
-            "chain_us": round(t_chain * 1e3, 1),
+            "ttm_us_cold": round(t_ttm * 1e3, 1),
+            "ttm_frac_hbm_cold": round(8 * (10771200 + 528 + 5222400) / (t_ttm * 1e-3) / 1e9 / peak, 3),
+            "ttm_us_l2warm": round(t_ttm_warm * 1e3, 1),
+            "norm_us_cold": round(t_nrm * 1e3, 1),
+            "norm_frac_hbm_cold": round(8 * 5222400 / (t_nrm * 1e-3) / 1e9 / peak, 3),
+            "norm_us_l2warm": round(t_nrm_warm * 1e3, 1),
+            "chain_us_cold": round(t_chain * 1e3, 1),
             "chain_frac_hbm": round(chain_bytes / (t_chain * 1e-3) / 1e9 / peak, 3),
         }
         del A, C1, C2
@@ -465,8 +569,7 @@ def run_reference(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 storage, f64 arithmetic", "data": "synthetic (seeded)",
-        "config": {"workload": "cfg2: ttv q=1..4 x {first,last,perm} + inner + norm, f32 128^4",
-                   "inputs": "host RAM"},
+        "config": cfg2_config(world),
         "cpu_baseline": {"value": round(value, 2), "unit": "GB/s", "cores": nthreads, "kind": "port",
                          "sample": "full cfg2 step per timed step (oracle/tl_oracle.c, OpenMP over outputs)"},
         "e2e": {"value": round(value, 2), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -539,27 +642,16 @@ def main():
     value = replica_value(STEP_BYTES, world, ms)
 
     # end to end through the public API (pinned host buffers, copies inside)
-    e2e = None
+    e2e = e2e_relayout = None
     if not args.no_e2e:
-        first_buf, first_layout = wl.host["first"]
-        wl.pinned = {"first": (torch.from_numpy(first_buf).pin_memory(), first_layout)}
+        wl.pinned = {name: (torch.from_numpy(buf).pin_memory(), layout) for name, (buf, layout) in wl.host.items()}
         wl.pinned_T2 = torch.from_numpy(wl.host_T2).pin_memory()
         wl.pinned_vecs = [torch.from_numpy(v).pin_memory() for v in wl.host_vecs]
-        wl.side_stream = torch.cuda.Stream()
-        for _ in range(args.warmup):  # also warms the pinned host-buffer cache
-            res = e2e_step(wl)
-            del res
-        barrier(world)
-        torch.cuda.synchronize()
-        te = time.perf_counter()
-        nE = max(1, min(5, args.steps))
-        for _ in range(nE):
-            h2d, d2h, res = e2e_step(wl)
-            del res
-        dt = (time.perf_counter() - te) / nE
-        dt = dist_max(dt, world)
-        e2e = {"value": round(world * STEP_BYTES / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+        wl.up_stream, wl.down_stream = torch.cuda.Stream(), torch.cuda.Stream()
+        e2e = time_e2e(wl, args.steps, args.warmup, world)
+        e2e_relayout = time_e2e(wl, args.steps, args.warmup, world, relayout_on_device=True)
+        e2e_relayout["note"] = "T and T2 uploaded; last-order and permuted copies made on the device (relayout)"
+        e2e["note"] = "the reference arm's inputs: three host layout buffers of T + T2 uploaded every step"
 
     if rank != 0:
         barrier(world)
@@ -579,9 +671,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f32 storage, f64 arithmetic (bit-exact ttv folds)",
         "data": "synthetic (seeded numpy PCG64; tests/workloads.py)",
-        "config": {"workload": "cfg2: ttv q=1..4 x {first,last,perm(3,1,2,4)} + inner + norm, f32 128^4 (1 GiB)",
-                   "step_bytes": STEP_BYTES, "l2": "inputs 1 GiB each > 126 MB L2 (no flush needed)",
-                   "parallelism": f"{world} independent replicas (weak scaling, no collective)"},
+        "config": cfg2_config(world),
         "roofline": {"bound": "hbm", "kernel": "ttv (12 launches/step, mean)", "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "algorithmic_bytes_per_launch": TTV_BYTES, "mean_launch_us": round(ttv_ms * 1e3, 2),
@@ -589,10 +679,11 @@ def main():
         "gpu_launches": 14 * args.steps,
         "clocks": clk,
         "e2e": e2e,
+        "e2e_device_relayout": e2e_relayout,
     }
     if not args.no_components:
         try:
-            line["components"] = components(args)
+            line["components"] = components(args, wl)
         except Exception as exc:  # keep the headline line even if a component fails
             line["components"] = {"error": repr(exc)}
     if not args.no_cpu:

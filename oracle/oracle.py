@@ -52,6 +52,8 @@ def lib():
         L.tlo_ttm_f64.argtypes = [ctypes.c_int, _i64p, _i64p, _f64p, ctypes.c_int64,
                                   ctypes.c_int64, ctypes.c_int64, _f64p, ctypes.c_int, _f64p,
                                   _i64p, ctypes.c_int64, ctypes.c_int]
+        L.tlo_ttm_canon_f64.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _f64p, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, _f64p, _f64p, ctypes.c_int, ctypes.c_int]
         L.tlo_ttm_i64.argtypes = [ctypes.c_int, _i64p, _i64p, _i64p, ctypes.c_int64,
                                   ctypes.c_int64, ctypes.c_int64, _i64p, ctypes.c_int, _i64p,
                                   _i64p, ctypes.c_int64, ctypes.c_int]
@@ -304,3 +306,25 @@ def transpose(abuf, shape, strides, tau, kind="float64"):
         pa = sum(ic[r] * strides[t - 1] for r, t in enumerate(tau))
         out[sum(i * w for i, w in zip(ic, fs))] = a[pa]
     return out, out_shape
+
+
+def ttm_canon(buf, shape, layout, bmat, bshape, bstrides, mode, absval=False, nthreads=0):
+    """Full-size ttm restatement (tlo_ttm_canon_f64): the output buffer in
+    A's OWN layout (extent J at ``mode``), every element the reference's
+    k-ordered mul-then-add fold; bit-identical to ``ttm``.  With absval the
+    fold of |A| |B| (the elementwise error bound)."""
+    shape = tuple(int(n) for n in shape)
+    layout = tuple(int(x) for x in layout)
+    t = layout.index(mode)
+    I = int(np.prod([shape[q - 1] for q in layout[:t]], dtype=np.int64)) if t else 1
+    K = shape[mode - 1]
+    O = int(np.prod(shape, dtype=np.int64)) // (I * K)
+    J = int(bshape[0])
+    a = _flat(np.asarray(buf), np.float64)
+    bm = _flat(bmat, np.float64)
+    c = np.empty(O * J * I, dtype=np.float64)
+    rc = lib().tlo_ttm_canon_f64(O, K, I, _ptr(a, "f64"), J, int(bstrides[0]), int(bstrides[1]), _ptr(bm, "f64"),
+                                 _ptr(c, "f64"), 1 if absval else 0, nthreads)
+    if rc != 0:
+        raise ValueError("oracle ttm_canon: invalid arguments")
+    return c

@@ -1,7 +1,7 @@
 """GPU coverage beyond the golden fixtures: edge shapes for every kernel
 regime, all ttm paths, the container API (relayout/assign/equality/
 interchange), error behaviour, allocation discipline, CUDA-graph capture,
-and full-size config-3 ttm checked on sampled outputs."""
+and full-size config-3 ttm checked on every output."""
 
 import random
 
@@ -11,6 +11,7 @@ import torch
 
 import workloads as W
 from oracle import oracle as O
+from tolerance import check_inner, check_ttm
 
 pytestmark = pytest.mark.gpu
 
@@ -122,7 +123,7 @@ def test_ttm_float64_paths(gpu, case):
     shape, layout, mode, J, blayout = case
     got, want, (buf, shape, st, mbuf, mshape, bst) = ttm_case(shape, layout, mode, J, blayout, "float64", 5)
     bound = O.ttm(np.abs(buf), shape, st, np.abs(mbuf), mshape, bst, mode)
-    assert np.all(np.abs(got - want) <= 1e-12 * bound)
+    check_ttm(got, want, bound)
 
 
 @pytest.mark.parametrize("dtype", ["int64", "float32"])
@@ -151,22 +152,34 @@ def test_ttm_float32_gett_bit_exact(gpu, case):
     assert np.array_equal(bits(got), bits(want.astype(np.float32))), case
 
 
-@pytest.mark.parametrize("q,layout", [(1, (1, 2, 3)), (2, (1, 2, 3)), (3, (1, 2, 3)),
-                                      (1, (3, 2, 1)), (2, (3, 2, 1)), (3, (3, 2, 1))])
-def test_cfg3_ttm_full_size_sampled(gpu, q, layout):
-    """Config 3 at full size: 4096 sampled outputs vs the oracle's k-order fold,
-    plus linearity in B, within 1e-12 of sum|A||B|."""
+@pytest.mark.parametrize("layout", [(1, 2, 3), (3, 2, 1)])
+@pytest.mark.parametrize("q", [1, 2, 3])
+def test_cfg3_ttm_full_size(gpu, q, layout):
+    """Config 3 at full size: all 100.7M outputs of each of the 6 cases against
+    the oracle's k-order fold (the canonical-form restatement, bit-identical
+    to the reference's fold; OpenMP on the host), each within 1e-12 of
+    sum_k |A||B| and the whole output within 1e-12 normwise; plus
+    linearity in B.  The observed maxima go to $TL_PARITY_REPORT if set."""
     A_, B_ = W.cfg3()
     buf = W.layout_buffer(A_, layout)
-    st = W.compute_strides(A_.shape, layout)
     mbuf = W.layout_buffer(B_, (1, 2))
     A = dev(buf, A_.shape, layout)
     Bm = dev(mbuf, B_.shape, (1, 2))
     C = tl().ttm(A, Bm, q).numpy()
-    sel = np.random.default_rng(q).integers(0, C.size, size=4096)
-    want = O.ttm(buf, A_.shape, st, mbuf, B_.shape, (1, 384), q, select=sel)
-    bound = O.ttm(np.abs(buf), A_.shape, st, np.abs(mbuf), B_.shape, (1, 384), q, select=sel)
-    assert np.all(np.abs(C[sel] - want) <= 1e-12 * bound)
+    out_shape = list(A_.shape)
+    out_shape[q - 1] = B_.shape[0]
+    out_shape = tuple(out_shape)
+    del A_
+    first = lambda canon: W.from_buffer(canon, out_shape, layout).ravel(order="F")  # noqa: E731
+    want = first(O.ttm_canon(buf, (512, 512, 512), layout, mbuf, B_.shape, (1, 384), q))
+    bound = first(O.ttm_canon(buf, (512, 512, 512), layout, mbuf, B_.shape, (1, 384), q, absval=True))
+    ratio, normwise = check_ttm(C, want, bound)
+    report = os.environ.get("TL_PARITY_REPORT")
+    if report:
+        with open(report, "a") as f:
+            f.write(json.dumps({"case": f"cfg3 q={q} layout={layout}", "outputs": int(C.size),
+                                "max_abs_err_over_bound": ratio, "normwise_rel_err": normwise}) + "\n")
+    del want, bound
     # linearity: ttm(A, 2B) == 2 ttm(A, B) exactly (scaling by 2 is exact)
     C2 = tl().ttm(A, dev(2.0 * mbuf, B_.shape, (1, 2)), q).numpy()
     assert np.array_equal(C2, 2.0 * C)
@@ -189,8 +202,8 @@ def test_inner_norm_layout_mix(gpu):
             if dtype == "int64":
                 assert got == want
             else:
-                bound = float(np.sum(np.abs(Ta.astype(np.float64)) * np.abs(Tb.astype(np.float64))))
-                assert abs(got - want) <= 1e-12 * bound
+                # same abstract tensors in every layout: the exact dot is layout-free
+                check_inner(got, want, Ta.ravel("F"), Tb.ravel("F"))
         if dtype != "int64":
             A = dev(W.layout_buffer(Ta, (3, 1, 4, 2)), shape, (3, 1, 4, 2))
             n = tl().frobenius_norm(A)

@@ -14,6 +14,7 @@ import pytest
 
 import workloads as W
 from oracle import oracle as O
+from tolerance import check_ttm
 
 pytestmark = pytest.mark.gpu
 
@@ -89,7 +90,7 @@ def test_fuzz_ttm(gpu, seed):
         want = O.ttm(buf, shape, st, mbuf, M.shape, bst, mode)
         if kind == "float64":
             bound = O.ttm(np.abs(buf), shape, st, np.abs(mbuf), M.shape, bst, mode)
-            assert np.all(np.abs(C - want) <= 1e-12 * bound), (shape, layout, mode, J)
+            check_ttm(C, want, bound)
         else:
             if kind == "float32":
                 want = want.astype(np.float32)
@@ -148,4 +149,4 @@ def test_fuzz_ttm_small_j_first_order(gpu, seed):
         st, bst = W.compute_strides(shape, layout), W.compute_strides(M.shape, (1, 2))
         want = O.ttm(buf, shape, st, mbuf, M.shape, bst, mode)
         bound = O.ttm(np.abs(buf), shape, st, np.abs(mbuf), M.shape, bst, mode)
-        assert np.all(np.abs(C - want) <= 1e-12 * bound), (shape, mode, J)
+        check_ttm(C, want, bound)

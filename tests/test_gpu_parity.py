@@ -14,6 +14,7 @@ import torch
 
 import workloads as W
 from oracle import oracle as O
+from tolerance import check_inner, check_ttm
 
 pytestmark = pytest.mark.gpu
 
@@ -75,7 +76,7 @@ def test_ttm_golden(gpu, small_golden):
             bstr = W.compute_strides(c["bshape"], c["blayout"])
             bound = O.ttm(np.abs(c["a"]), c["shape"], W.compute_strides(c["shape"], c["layout"]),
                           np.abs(c["bmat"]), c["bshape"], bstr, c["mode"])
-            assert np.all(np.abs(got - want) <= RTOL64 * bound + 1e-300), c
+            check_ttm(got, want, bound)
 
 
 def test_inner_norm_golden(gpu, small_golden):
@@ -87,9 +88,9 @@ def test_inner_norm_golden(gpu, small_golden):
             if c["kind"] == "int64":
                 assert got == c["value"] and isinstance(got, int)
             else:
-                bound = O.inner(np.abs(c["a"]), c["shape"], W.compute_strides(c["shape"], c["layout"]),
-                                np.abs(c["b"]), W.compute_strides(c["shape"], c["blayout"]))
-                assert abs(got - c["value"]) <= RTOL64 * bound, c
+                shp = tuple(c["shape"])
+                check_inner(got, c["value"], W.from_buffer(c["a"], shp, c["layout"]).ravel(order="F"),
+                            W.from_buffer(c["b"], shp, c["blayout"]).ravel(order="F"))
         elif c["op"] == "norm":
             A = dev_tensor(c["a"], c["shape"], c["layout"])
             got = tl().frobenius_norm(A)

@@ -240,3 +240,29 @@ def test_product_package_never_touches_the_oracle():
             text = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in text, fn
             assert "tl_oracle" not in text and "libtloracle" not in text, fn
+
+
+def test_exact_dot_matches_fractions():
+    """The normwise inner-product reference (tests/tolerance.py) is exact."""
+    import fractions
+
+    import numpy as np
+    from tolerance import exact_dot
+
+    rng = np.random.default_rng(7)
+    for n in (1, 7, 300):
+        a, b = rng.standard_normal(n) * 1e3, rng.standard_normal(n) * 1e-3
+        want = float(sum(fractions.Fraction(x) * fractions.Fraction(y) for x, y in zip(a, b)) + fractions.Fraction(0.5))
+        assert exact_dot(a, b, 0.5) == want
+
+
+def test_walk_positions_host_cursor():
+    """Iterator bookkeeping needs no device: the reference recursion's visit
+    order (iterators.py:165-182) over a host-list cursor."""
+    from paper_1711_10912_b200 import MultiIterator, walk_positions
+
+    it = MultiIterator([0] * 24, 0, (1, 4, 12), (4, 3, 2))
+    assert walk_positions(it) == list(range(24))
+    it = MultiIterator([0] * 24, 1, (6, 1), (4, 2))
+    assert walk_positions(it) == [1 + 6 * i + j for j in range(2) for i in range(4)]
+    assert it.begin(1).stride == 1 and it.end(0).pos == 1 + 24

@@ -50,6 +50,24 @@ def test_oracle_ttm_small(small_golden):
     assert n >= 60
 
 
+def test_oracle_ttm_canon_small(small_golden):
+    """The full-size (canonical-form, vectorised) ttm restatement equals the
+    reference's outputs bit for bit on every float golden case."""
+    n = 0
+    for c in small_golden["cases"]:
+        if c["op"] != "ttm" or np.asarray(c["a"]).dtype.kind != "f":
+            continue
+        bstr = W.compute_strides(c["bshape"], c["blayout"])
+        layout = tuple(c["layout"])
+        got = O.ttm_canon(c["a"], c["shape"], layout, c["bmat"], c["bshape"], bstr, c["mode"])
+        out_shape = list(c["shape"])
+        out_shape[c["mode"] - 1] = c["bshape"][0]
+        first = W.from_buffer(got, tuple(out_shape), layout).ravel(order="F")
+        assert first.tobytes() == np.asarray(c["out"], dtype=np.float64).tobytes(), c
+        n += 1
+    assert n >= 20
+
+
 def test_oracle_inner_norm_small(small_golden):
     for c in small_golden["cases"]:
         if c["op"] == "inner":

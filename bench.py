@@ -390,23 +390,41 @@ def components(args, wl=None):
 
     flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
-    def cold(fn, iters=7, warm=2):
-        """Median device time of one launch with a cold L2: a 512 MB write
-        (4x L2) runs before each timed launch, outside its events (the host
-        enqueues the launch while the flush runs, so no launch gap)."""
-        for _ in range(warm):
+    def cold(fn, reps=20, iters=5):
+        """Device time of one launch with a cold L2: a CUDA graph of `reps`
+        x [512 MB write (4x L2), fn] minus a graph of `reps` x [the same
+        write], divided by `reps` -- no event or host launch overhead in the
+        number (an event pair around a single eager launch adds ~6 us on
+        this box: tools/experiments/red_probe.cu)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
             fn()
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        ts = []
+        graphs = []
+        for with_fn in (True, False):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for r in range(reps):
+                    flush_buf.fill_(float(r))
+                    if with_fn:
+                        fn()
+            graphs.append(g)
+        ts = {True: [], False: []}
         for _ in range(iters):
-            flush_buf.fill_(float(len(ts)))
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
+            for with_fn, g in zip((True, False), graphs):
+                g.replay()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                g.replay()
+                b.record()
+                torch.cuda.synchronize()
+                ts[with_fn].append(a.elapsed_time(b))
+        del graphs
+        return (statistics.median(ts[True]) - statistics.median(ts[False])) / reps
 
     def med_eager(fn, iters=5, warm=2):
         for _ in range(warm):

@@ -4,7 +4,7 @@
 # -> gpurun_out/TAG_times.csv + a one-line-per-kernel summary on stdout.
 set -u
 tag=$1; regex=$2; shift 2
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none ${NCU_EXTRA:-} \
     -k "regex:${regex}" --csv --log-file gpurun_out/${tag}_times.csv "$@" > gpurun_out/${tag}_cmd.log 2>&1
 python - "$tag" <<'PY'
 import csv, sys, collections

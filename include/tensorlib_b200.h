@@ -113,6 +113,22 @@ int tl_inner_flat(const tl_desc *a, const void *a_ptr, const tl_desc *b, const v
 int tl_frobenius_norm(const tl_desc *a, const void *a_ptr, double *result_dev,
                       void *ws, size_t ws_bytes, void *stream);
 
+/* times_vectors -- contraction.py:481-519 (explicit-modes form) as ONE
+ * cooperative launch: the vectors are applied highest mode first, each step
+ * the reference's left fold over k, each intermediate rounded to A's
+ * storage type -- bit-identical to the sequence of tl_ttv calls.  modes:
+ * one-based, strictly increasing, one per vector (an order-1 remainder is
+ * folded like the reference's inner_product_flat).  c: dense first-order,
+ * A's float dtype.  Returns TL_EUNSUPPORTED (nothing enqueued) when a step's
+ * output is a permutation of its canonical order (e.g. last-order A) or A
+ * is not floating; the caller then issues the tl_ttv sequence.  Scratch for
+ * the intermediates: tl_times_vectors_workspace_bytes. */
+int tl_times_vectors_workspace_bytes(const tl_desc *a, int32_t nvec, const int32_t *modes,
+                                     const tl_desc *vdescs, size_t *ws_bytes);
+int tl_times_vectors(const tl_desc *a, const void *a_ptr, int32_t nvec, const int32_t *modes,
+                     const tl_desc *vdescs, const void *const *vptrs, const tl_desc *c, void *c_ptr,
+                     void *ws, size_t ws_bytes, void *stream);
+
 /* hopm -- hopm.py:63-120.  Gauss-Seidel higher-order power method, run
  * entirely on the device.  u_ptrs[r] (r < p) are device float64 vectors of
  * length n_{r+1}: on entry the (already normalised) start vectors, on exit

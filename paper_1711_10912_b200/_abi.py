@@ -42,6 +42,8 @@ EXPORTS = (
     "tl_rank_one_compose",
     "tl_residual",
     "tl_plan_describe",
+    "tl_times_vectors_workspace_bytes",
+    "tl_times_vectors",
 )
 
 
@@ -106,10 +108,13 @@ def load_library(path: str = LIB_PATH):
         L.tl_copy.argtypes = [_dp, _vp, _dp, _vp, _vp]
         L.tl_rank_one_compose.argtypes = [_dp, vpp, _vp, _vp, _vp]
         L.tl_residual.argtypes = [_dp, _vp, vpp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.tl_times_vectors_workspace_bytes.argtypes = [_dp, ctypes.c_int32, i32p, _dp, ctypes.POINTER(ctypes.c_size_t)]
+        L.tl_times_vectors.argtypes = [_dp, _vp, ctypes.c_int32, i32p, _dp, vpp, _dp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_plan_describe.argtypes = [ctypes.c_int32, _dp, _dp, ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
         for name in ("tl_ttv", "tl_ttm", "tl_inner", "tl_inner_flat", "tl_frobenius_norm", "tl_hopm_workspace_bytes", "tl_hopm",
                      "tl_hopm_graph_create", "tl_graph_launch", "tl_graph_destroy", "tl_copy", "tl_rank_one_compose",
-                     "tl_residual", "tl_plan_describe"):
+                     "tl_residual", "tl_plan_describe", "tl_times_vectors_workspace_bytes", "tl_times_vectors"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L

@@ -1,3 +1,4 @@
+#include <algorithm>
 // abi.cu -- extern "C" entry points of libtlb200.so (include/tensorlib_b200.h).
 //
 // Argument checks mirror the reference's errors (contraction.py:123-127,
@@ -35,6 +36,8 @@ int hopm_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u0, d
                  double tol, double *l, double *hist, int32_t *info, double *resid, void *ws, size_t ws_bytes,
                  cudaStream_t st);
 void copy_preload();
+int chain_enqueue(int n, const tl_desc *descs, const void *const *srcs, void *const *outs, const int *modes,
+                  const void *const *bptrs, const int32_t *bdtypes, const int64_t *bstrides, cudaStream_t st);
 int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_ptr, cudaStream_t st);
 int rank_one_enqueue(const tl_desc &shape, const double *const *u, const double *scale_dev, double *out,
                      cudaStream_t st);
@@ -439,6 +442,120 @@ int tl_copy(const tl_desc *a, const void *a_ptr, const tl_desc *c, void *c_ptr, 
     }
     if (!check_ptrs("copy", {a_ptr, c_ptr})) return TL_EINVAL;
     return copy_enqueue(*a, a_ptr, *c, c_ptr, (cudaStream_t)stream);
+}
+
+
+// ---------------------------------------------------------------- times_vectors
+// The chain of a times_vectors call (contraction.py:481-519): vectors sorted
+// by mode, highest first; each step contracts one mode of the previous
+// first-order result; an order-1 remainder is contracted as an (n, 1)
+// column over mode 1 (the reference's inner_product_flat fold).
+struct TvChain {
+    int n = 0;
+    tl_desc in[TL_MAX_ORDER];
+    int m0[TL_MAX_ORDER];
+    int vec[TL_MAX_ORDER];  // index into the caller's vector arrays
+    int64_t inter_elems = 0;  // largest intermediate (ping-pong halves of the workspace)
+};
+
+static int tv_plan(const tl_desc *a, int32_t nvec, const int32_t *modes, const tl_desc *vdescs, TvChain &ch) {
+    if (!check_desc(a, "times_vectors A")) return TL_EINVAL;
+    const int p = a->order;
+    if (nvec < 1 || nvec > p || modes == nullptr || vdescs == nullptr) {
+        set_error("times_vectors: %d vectors for order %d", nvec, p);
+        return TL_EINVAL;
+    }
+    int order[TL_MAX_ORDER];
+    for (int q = 0; q < nvec; ++q) {
+        order[q] = q;
+        if (modes[q] < 1 || modes[q] > p) {
+            set_error("times_vectors: mode %d out of range 1..%d", modes[q], p);
+            return TL_EINVAL;
+        }
+        if (q && modes[q] <= modes[q - 1]) {
+            set_error("times_vectors: modes must be strictly increasing");
+            return TL_EINVAL;
+        }
+    }
+    std::sort(order, order + nvec, [&](int x, int y) { return modes[x] > modes[y]; });
+    tl_desc cur = *a;
+    for (int s = 0; s < nvec; ++s) {
+        const int q = order[s];
+        int m0 = modes[q] - 1;
+        const tl_desc &v = vdescs[q];
+        if (!check_desc(&v, "times_vectors vector")) return TL_EINVAL;
+        if (cur.order == 1) {  // (n, 1) column over mode 1
+            cur.order = 2;
+            cur.extent[1] = 1;
+            cur.stride[1] = cur.extent[0];
+            m0 = 0;
+        }
+        if (!(v.order == 1 || (v.order == 2 && v.extent[1] == 1)) || v.extent[0] != cur.extent[m0]) {
+            set_error("times_vectors vector %d does not match extent %lld", q + 1, (long long)cur.extent[m0]);
+            return TL_EINVAL;
+        }
+        ch.in[s] = cur;
+        ch.m0[s] = m0;
+        ch.vec[s] = q;
+        // next input: cur without dimension m0, first-order float
+        tl_desc nx{};
+        nx.order = cur.order - 1;
+        nx.dtype = a->dtype;
+        int64_t run = 1;
+        for (int r = 0, t = 0; r < cur.order; ++r) {
+            if (r == m0) continue;
+            nx.extent[t] = cur.extent[r];
+            nx.stride[t] = run;
+            run *= cur.extent[r];
+            ++t;
+        }
+        if (s + 1 < nvec) ch.inter_elems = std::max<int64_t>(ch.inter_elems, run);
+        cur = nx;
+    }
+    ch.n = nvec;
+    return TL_OK;
+}
+
+int tl_times_vectors_workspace_bytes(const tl_desc *a, int32_t nvec, const int32_t *modes, const tl_desc *vdescs,
+                                     size_t *bytes) {
+    TvChain ch;
+    int rc = tv_plan(a, nvec, modes, vdescs, ch);
+    if (rc != TL_OK) return rc;
+    if (bytes == nullptr) return TL_EINVAL;
+    *bytes = 2 * (((size_t)ch.inter_elems * dtype_size(a->dtype) + 255) & ~(size_t)255);
+    return TL_OK;
+}
+
+int tl_times_vectors(const tl_desc *a, const void *a_ptr, int32_t nvec, const int32_t *modes, const tl_desc *vdescs,
+                     const void *const *vptrs, const tl_desc *c, void *c_ptr, void *ws, size_t ws_bytes, void *stream) {
+    TvChain ch;
+    int rc = tv_plan(a, nvec, modes, vdescs, ch);
+    if (rc != TL_OK) return rc;
+    if (!check_desc(c, "times_vectors C") || vptrs == nullptr) return TL_EINVAL;
+    if (!check_ptrs("times_vectors", {a_ptr, c_ptr})) return TL_EINVAL;
+    const size_t half = ((size_t)ch.inter_elems * dtype_size(a->dtype) + 255) & ~(size_t)255;
+    if (nvec > 1 && (ws == nullptr || ws_bytes < 2 * half)) {
+        set_error("times_vectors: workspace of %zu bytes required", 2 * half);
+        return TL_EWORKSPACE;
+    }
+    const void *srcs[TL_MAX_ORDER];
+    void *outs[TL_MAX_ORDER];
+    const void *bp[TL_MAX_ORDER];
+    int32_t bdt[TL_MAX_ORDER];
+    int64_t bst[TL_MAX_ORDER];
+    for (int s = 0; s < ch.n; ++s) {
+        srcs[s] = s == 0 ? a_ptr : outs[s - 1];
+        outs[s] = (s + 1 == ch.n) ? c_ptr : (void *)((unsigned char *)ws + (s % 2) * half);
+        const tl_desc &v = vdescs[ch.vec[s]];
+        bp[s] = (const unsigned char *)vptrs[ch.vec[s]] + v.offset * (int64_t)dtype_size(v.dtype);
+        bdt[s] = v.dtype;
+        bst[s] = v.stride[0];
+        if (vptrs[ch.vec[s]] == nullptr) {
+            set_error("times_vectors: null vector pointer");
+            return TL_EINVAL;
+        }
+    }
+    return chain_enqueue(ch.n, ch.in, srcs, outs, ch.m0, bp, bdt, bst, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -510,3 +510,38 @@ def test_hopm_float32_equals_widened_float64(gpu):
         s64 = m.hopm(a64, max_sweeps=8, tol=0.0)
         assert s32.lambda_history == s64.lambda_history
         assert all(np.array_equal(x.numpy(), y.numpy()) for x, y in zip(s32.u, s64.u))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_times_vectors_chain_equals_launch_sequence(gpu, dtype, monkeypatch):
+    """The one-launch chain (tl_times_vectors) is bit-identical to the ttv
+    sequence, on every layout (permuted steps fall back to the sequence)."""
+    m = tl()
+    rng = random.Random(77)
+    nrng = np.random.default_rng(77)
+    for _ in range(40):
+        p = rng.randint(2, 5)
+        shape = tuple(rng.randint(1, 9) for _ in range(p))
+        layout = tuple(range(1, p + 1)) if rng.random() < 0.6 else W.random_layout(p, rng.randint(0, 99))
+        k = rng.randint(2, p)
+        modes = sorted(rng.sample(range(1, p + 1), k))
+        T = nrng.uniform(-1, 1, size=shape).astype(dtype)
+        A = m.DenseTensor.from_memory(shape, W.layout_buffer(T, layout), layout=layout)
+        vs = [m.DenseTensor.from_memory((shape[q - 1],), nrng.uniform(-1, 1, size=shape[q - 1])) for q in modes]
+        monkeypatch.setenv("TL_TV_CHAIN", "1")
+        got = m.times_vectors(A, vs, modes)
+        monkeypatch.setenv("TL_TV_CHAIN", "0")
+        want = m.times_vectors(A, vs, modes)
+        assert got.shape == want.shape and got.dtype == want.dtype
+        assert got.numpy().tobytes() == want.numpy().tobytes(), (shape, layout, modes)
+    # larger: a 400^3-shaped chain and a 1 GiB-class float32 chain shape (smaller here)
+    for shape, modes, dt in (((400, 400, 40), (2, 3), "float64"), ((64, 64, 64, 64), (2, 3, 4), "float32"),
+                             ((64, 64, 64, 64), (1, 2, 3, 4), "float32")):
+        T = nrng.uniform(-1, 1, size=shape).astype(dt)
+        A = m.DenseTensor.from_memory(shape, T.ravel(order="F"))
+        vs = [m.DenseTensor.from_memory((shape[q - 1],), nrng.uniform(-1, 1, size=shape[q - 1])) for q in modes]
+        monkeypatch.setenv("TL_TV_CHAIN", "1")
+        got = m.times_vectors(A, vs, modes).numpy()
+        monkeypatch.setenv("TL_TV_CHAIN", "0")
+        want = m.times_vectors(A, vs, modes).numpy()
+        assert got.tobytes() == want.tobytes(), (shape, modes)

@@ -24,6 +24,7 @@ struct CopyParams {
     // tiled transpose: X = destination's fastest dim, Y = source's fastest
     int64_t nX, nY, n_rest, a_sX, a_sY, c_sY, tiles_x, tiles_y;
     DigitMap rest_a, rest_c;
+    DigitMap64 amap64, cmap64;  // past 2^32 elements: the generic 64-bit copy
 };
 
 template <class T> __global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyParams P) {
@@ -32,6 +33,14 @@ template <class T> __global__ void __launch_bounds__(256) copy_kernel(const __gr
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P.n; q += stride)
         c[P.cmap.map((uint32_t)q)] = a[P.amap.map((uint32_t)q)];
+}
+
+template <class T> __global__ void __launch_bounds__(256) copy64_kernel(const __grid_constant__ CopyParams P) {
+    const T *a = (const T *)P.a;
+    T *c = (T *)P.c;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P.n; q += stride)
+        c[P.cmap64.map((uint64_t)q)] = a[P.amap64.map((uint64_t)q)];
 }
 
 template <class T> __global__ void __launch_bounds__(256) copy_tiled_kernel(const __grid_constant__ CopyParams P) {
@@ -114,6 +123,8 @@ template <class T> static cudaError_t launch_copy(const CopyParams &P, int kind,
         copy_tiled_vec_kernel<T><<<grid, 256, 0, st>>>(P);
     else if (kind == 1)
         copy_tiled_kernel<T><<<grid, 256, 0, st>>>(P);
+    else if (kind == 3)
+        copy64_kernel<T><<<grid, 256, 0, st>>>(P);
     else
         copy_kernel<T><<<grid, 256, 0, st>>>(P);
     return cudaGetLastError();
@@ -143,10 +154,6 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
     P.c = (unsigned char *)c_ptr + c.offset * (int64_t)s;
     P.n = volume(c);
     if (P.n == 0) return TL_OK;
-    if (P.n > 0xffffffffll) {
-        set_error("copy: more than 2^32 elements");
-        return TL_EUNSUPPORTED;
-    }
     // source's fastest (smallest |stride|) non-trivial dimension
     int Y = -1;
     for (int r = 0; r < a.order; ++r)
@@ -163,7 +170,12 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
         if (same)
             return cuda_status(cudaMemcpyAsync(P.c, P.a, (size_t)P.n * s, cudaMemcpyDeviceToDevice, st), "copy");
     }
-    if (X >= 0 && Y >= 0 && X != Y && c.extent[X] >= 8 && c.extent[Y] >= 8) {
+    // the tiled transposes index tiles in 64 bits and the rest digits in 32
+    bool rest32 = true;
+    for (int r = 0; r < c.order; ++r)
+        if (r != X && r != Y && c.extent[r] > kIdx32) rest32 = false;
+    if (rest32 && X >= 0 && Y >= 0) rest32 = volume(c) / (c.extent[X] * c.extent[Y]) <= kIdx32;
+    if (X >= 0 && Y >= 0 && X != Y && c.extent[X] >= 8 && c.extent[Y] >= 8 && rest32) {
         kind = 1;
         P.nX = c.extent[X];
         P.nY = c.extent[Y];
@@ -208,9 +220,15 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
                 la.push_back({c.extent[r], a.stride[r]});
             }
         }
-        build_map(la, P.amap);
-        build_map(lc, P.cmap);
         grid = std::min<int64_t>((P.n + 255) / 256, (int64_t)di.num_sms * 16);
+        if (P.n > kIdx32) {
+            kind = 3;  // 2^32+ elements: 64-bit digit maps
+            build_map64(la, P.amap64);
+            build_map64(lc, P.cmap64);
+        } else {
+            build_map(la, P.amap);
+            build_map(lc, P.cmap);
+        }
     }
     cudaError_t e;
     if (s == 4) e = launch_copy<float>(P, kind, (int)grid, st);

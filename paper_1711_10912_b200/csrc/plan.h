@@ -70,6 +70,16 @@ inline bool build_map(const DigitList &dl, DigitMap &m) {
     return true;
 }
 
+inline void build_map64(const DigitList &dl, DigitMap64 &m) {
+    m.n = (int32_t)dl.size();
+    for (size_t d = 0; d < dl.size(); ++d) {
+        m.ext[d] = dl[d].first;
+        m.stride[d] = dl[d].second;
+    }
+}
+
+constexpr int64_t kIdx32 = 0xffffffffll;  // largest index the 32-bit digit maps take
+
 struct Canon {
     int64_t O = 1, K = 1, I = 1;
     int64_t jstride = 0;  // ttm: output stride of the new mode's index j

@@ -105,6 +105,9 @@ struct ReduceParams {
     int64_t a_sY, b_sX;  // a's stride along Y, b's stride along X
     DigitMap rest_a, rest_b;
     int64_t tiles_x, tiles_y;
+    // past 2^32 rows / tiles: a's memory order e -> b's offset
+    int64_t n_elem;
+    DigitMap64 b64;
 };
 
 // Block-level reduction of one accumulator per thread; returns the CTA sum
@@ -382,6 +385,25 @@ __global__ void __launch_bounds__(256) dot_tiled_vec_kernel(const __grid_constan
     finish(P, acc);
 }
 
+// ------------------------------------------------------------ past 2^32
+// Index ranges beyond the 32-bit maps (2^33+ elements with short rows or
+// tiles): a is walked in its memory order, b's offset of the same element
+// comes from a 64-bit digit map; same accumulators and combine.
+template <class TA, class TB>
+__global__ void __launch_bounds__(256) dot_generic64_kernel(const __grid_constant__ ReduceParams P) {
+    using Acc = typename RedAcc<TA>::type;
+    ThreadAcc<TA> ta;
+    ta.zero();
+    const TA *a = (const TA *)P.a;
+    const TB *b = (const TB *)P.b;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    int j = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < P.n_elem; e += nth, ++j)
+        ta.add(j, as_acc(__ldcs(a + e)), as_acc(__ldcs(b + P.b64.map((uint64_t)e))));
+    Acc acc = block_reduce(ta.total());
+    finish(P, acc);
+}
+
 size_t reduce_workspace_bytes();
 
 // ------------------------------------------------------------ rank one / residual
@@ -585,6 +607,26 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
     if (N == 0) {
         set_error("inner: empty tensor");
         return TL_EINVAL;
+    }
+    {
+        // index ranges past the 32-bit maps: the generic 64-bit walk
+        DigitList dl;
+        for (int r : da) dl.push_back({a.extent[r], b.stride[r]});
+        DigitList col = collapse(dl);
+        bool big = N > kIdx32 && col.size() > 1;
+        for (auto &dg : col) big = big || dg.first > kIdx32;
+        if (big) {
+            P.n_elem = N;
+            build_map64(col, P.b64);
+            const int64_t grid = std::min<int64_t>((N + threads - 1) / threads, std::min<int64_t>((int64_t)di.num_sms * 4, kMaxPartials));
+            const unsigned G = (unsigned)grid;
+            if (a.dtype == TL_F32 && b.dtype == TL_F32) dot_generic64_kernel<float, float><<<G, threads, 0, st>>>(P);
+            else if (a.dtype == TL_F64 && b.dtype == TL_F64) dot_generic64_kernel<double, double><<<G, threads, 0, st>>>(P);
+            else if (a.dtype == TL_F32 && b.dtype == TL_F64) dot_generic64_kernel<float, double><<<G, threads, 0, st>>>(P);
+            else if (a.dtype == TL_F64 && b.dtype == TL_F32) dot_generic64_kernel<double, float><<<G, threads, 0, st>>>(P);
+            else dot_generic64_kernel<int64_t, int64_t><<<G, threads, 0, st>>>(P);
+            return cuda_status(cudaGetLastError(), "inner/norm (64-bit index) launch");
+        }
     }
     if (same_fast) {
         // digits of a's memory order with b's strides; rows along the shared fastest dim

@@ -70,6 +70,29 @@ struct DigitMap {
     }
 };
 
+// The same map for index spaces past 2^32 (any digit extent, 64-bit
+// numerators, native division): the generic fallback kernels for tensors
+// whose O, I or volume exceed the 32-bit maps above (the reference's index
+// cap is 2^63 - 1, layout.py:48).
+struct DigitMap64 {
+    int32_t n;
+    int64_t ext[TL_MAX_DIGITS];
+    int64_t stride[TL_MAX_DIGITS];
+
+    __device__ __forceinline__ int64_t map(uint64_t x) const {
+        int64_t off = 0;
+#pragma unroll 1
+        for (int d = 0; d < n - 1; ++d) {
+            const uint64_t e = (uint64_t)ext[d];
+            const uint64_t q = x / e;
+            off += (int64_t)(x - q * e) * stride[d];
+            x = q;
+        }
+        if (n > 0) off += (int64_t)x * stride[n - 1];
+        return off;
+    }
+};
+
 // ------------------------------------------------------------------ dtypes
 template <class T> struct AccOf { using type = double; };
 template <> struct AccOf<int64_t> { using type = int64_t; };

@@ -36,6 +36,9 @@ struct TtmSimtParams {
     int32_t R;
     int64_t ntiles;
     FastDiv I_div;
+    // index ranges past 2^32 (the one-thread-per-output kernel only)
+    int32_t big;
+    DigitMap64 in_map64, out_map64;
 };
 
 template <class T, class TC>
@@ -56,6 +59,8 @@ __global__ void __launch_bounds__(256) ttm_simt_kernel(const __grid_constant__ T
     int64_t off;
     if (P.ident)
         off = (o * P.J + j) * P.I + i;
+    else if (P.big)
+        off = P.out_map64.map((uint64_t)o) + j * P.jstride + P.in_map64.map((uint64_t)i);
     else
         off = P.out_map.map((uint32_t)o) + j * P.jstride + P.in_map.map((uint32_t)i);
     ((TC *)P.c)[off] = narrow<TC>(acc);
@@ -654,9 +659,12 @@ static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm,
     P.bs1 = bm.stride[1];
     P.jstride = cn.jstride;
     P.ident = cn.ident ? 1 : 0;
-    if (!build_map(cn.inner, P.in_map) || !build_map(cn.outer, P.out_map)) {
-        set_error("ttm: extent exceeds 32-bit digit range");
-        return false;
+    P.big = (cn.O > kIdx32 || cn.I > kIdx32) ? 1 : 0;
+    if (P.big || !build_map(cn.inner, P.in_map) || !build_map(cn.outer, P.out_map)) {
+        // past 2^32: only the one-thread-per-output kernel (64-bit maps) runs
+        P.big = 1;
+        build_map64(cn.inner, P.in_map64);
+        build_map64(cn.outer, P.out_map64);
     }
     return true;
 }
@@ -784,7 +792,7 @@ static bool plan_bulk(const TtmSimtParams &P, BulkPlan &bp) {
 // B image <= 48 KB, 16-byte aligned A); false -> the caller uses another path.
 static bool staged_family_ok(const TtmSimtParams &P, int32_t dtype) {
     const int64_t s = (int64_t)dtype_size(dtype);
-    return !(P.I > 256 || P.K * P.I * s > 32 * 1024 || P.J * P.K * 8 > 48 * 1024 || (uintptr_t)P.a % 16 != 0 ||
+    return !(P.big || P.I > 256 || P.K * P.I * s > 32 * 1024 || P.J * P.K * 8 > 48 * 1024 || (uintptr_t)P.a % 16 != 0 ||
              P.O > 0xffffffffll);
 }
 
@@ -939,6 +947,10 @@ int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     if (total == 0) return TL_OK;
     const int threads = 256;
     const int64_t grid = (total + threads - 1) / threads;
+    if (grid > 0x7fffffffll) {
+        set_error("ttm: %lld outputs exceed one launch", (long long)total);
+        return TL_EUNSUPPORTED;
+    }
     if (a.dtype == TL_F64) ttm_simt_kernel<double, double><<<(unsigned)grid, threads, 0, st>>>(P);
     else if (a.dtype == TL_F32) ttm_simt_kernel<float, float><<<(unsigned)grid, threads, 0, st>>>(P);
     else ttm_simt_kernel<int64_t, int64_t><<<(unsigned)grid, threads, 0, st>>>(P);

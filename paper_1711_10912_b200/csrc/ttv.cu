@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <numeric>
 #include <type_traits>
@@ -1419,10 +1420,17 @@ static const char *ttv_regime_name(const TtvLaunch &L) {
     }
 }
 
+static bool ttv_needs64(const Canon &cn);
+
 // Host-only description of the plan (tl_plan_describe).
 int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
     TtvLaunch L{};
     Canon cn;
+    if (canon_contraction(a, m0, 0, cn) && ttv_needs64(cn)) {
+        snprintf(buf, len, "{\"O\": %lld, \"K\": %lld, \"I\": %lld, \"ident\": %d, \"regime\": \"generic64\"}",
+                 (long long)cn.O, (long long)cn.K, (long long)cn.I, cn.ident ? 1 : 0);
+        return TL_OK;
+    }
     int rc = ttv_make_plan(a, (const void *)0x100000, m0, L, cn);
     if (rc != TL_OK) return rc;
     if (L.regime == 0) plan_box(cn, L, (int64_t)dtype_size(a.dtype), 0x100000, device_info().num_sms);
@@ -1467,6 +1475,76 @@ static bool small_cluster_fits(const TtvLaunch &L) {
     return clusters >= 1;
 }
 
+// ------------------------------------------------------------- past 2^32
+// Index ranges beyond the 32-bit digit maps (O or I >= 2^32, K >= 2^31, or
+// a digit that large -- tensors of 2^33+ elements, which a 180 GB B200 can
+// hold): one thread per output (o, i), 64-bit digit maps, the same k-ordered
+// fold.  Loads coalesce along i when I > 1.  Correctness path: the tuned
+// kernels above cover every tensor below that size.
+struct TtvParams64 {
+    const void *a;
+    const void *b;
+    void *c;
+    const int32_t *stop;
+    int64_t b_stride;
+    int32_t b_dtype;
+    int64_t O, K, I;
+    DigitMap64 in_map, out_map;
+};
+
+template <class TA, class TC>
+__global__ void __launch_bounds__(256) ttv_generic64_kernel(const __grid_constant__ TtvParams64 P) {
+    using Acc = typename AccOf<TA>::type;
+    if (stop_requested(P.stop)) return;
+    const TA *a = (const TA *)P.a;
+    const int64_t total = P.O * P.I;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += nth) {
+        const int64_t o = t / P.I, i = t - o * P.I;
+        const TA *x = a + o * P.K * P.I + i;
+        Acc acc = Acc(0);
+        for (int64_t k = 0; k < P.K; ++k) acc = fold_step(acc, (Acc)x[k * P.I], load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride));
+        ((TC *)P.c)[P.out_map.map((uint64_t)o) + P.in_map.map((uint64_t)i)] = narrow<TC>(acc);
+    }
+}
+
+static bool ttv_needs64(const Canon &cn) {
+    if (cn.O > kIdx32 || cn.I > kIdx32 || cn.K > 0x7fffffffll) return true;
+    for (auto &d : cn.inner)
+        if (d.first > kIdx32) return true;
+    for (auto &d : cn.outer)
+        if (d.first > kIdx32) return true;
+    return false;
+}
+
+static int ttv_generic64_enqueue(const tl_desc &a, const void *a_ptr, const Canon &cn, const void *b_ptr,
+                                 int32_t b_dtype, int64_t b_stride, int32_t c_dtype, void *c_ptr,
+                                 const int32_t *stop, cudaStream_t st) {
+    TtvParams64 P{};
+    P.a = (const unsigned char *)a_ptr + a.offset * (int64_t)dtype_size(a.dtype);
+    P.b = b_ptr;
+    P.c = c_ptr;
+    P.stop = stop;
+    P.b_stride = b_stride;
+    P.b_dtype = b_dtype;
+    P.O = cn.O;
+    P.K = cn.K;
+    P.I = cn.I;
+    build_map64(cn.inner, P.in_map);
+    build_map64(cn.outer, P.out_map);
+    if (P.O * P.I == 0) return TL_OK;
+    const int64_t grid = std::min<int64_t>((P.O * P.I + 255) / 256, (int64_t)device_info().num_sms * 16);
+    if (a.dtype == TL_F32 && c_dtype == TL_F32) ttv_generic64_kernel<float, float><<<(unsigned)grid, 256, 0, st>>>(P);
+    else if (a.dtype == TL_F32 && c_dtype == TL_F64) ttv_generic64_kernel<float, double><<<(unsigned)grid, 256, 0, st>>>(P);
+    else if (a.dtype == TL_F64 && c_dtype == TL_F64) ttv_generic64_kernel<double, double><<<(unsigned)grid, 256, 0, st>>>(P);
+    else if (a.dtype == TL_I64 && c_dtype == TL_I64) ttv_generic64_kernel<int64_t, int64_t><<<(unsigned)grid, 256, 0, st>>>(P);
+    else {
+        set_error("ttv: unsupported dtype combination (a=%d, c=%d)", a.dtype, c_dtype);
+        return TL_EUNSUPPORTED;
+    }
+    return cuda_status(cudaGetLastError(), "ttv (64-bit index) launch");
+}
+
 // Entry used by tl_ttv and by the HOPM orchestration (which passes a stop
 // flag and binary64 outputs for float32 storage).
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
@@ -1474,6 +1552,13 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
                 const FusedNorm *fn, bool pdl) {
     TtvLaunch L{};
     Canon cn;
+    if (canon_contraction(a, m0, 0, cn) && ttv_needs64(cn)) {
+        if (fn != nullptr && fn->enabled) {
+            set_error("hopm: index ranges past 2^32 are not supported by the fused normalisation");
+            return TL_EUNSUPPORTED;
+        }
+        return ttv_generic64_enqueue(a, a_ptr, cn, b_ptr, b_dtype, b_stride, c_dtype, c_ptr, stop, st);
+    }
     int rc = ttv_make_plan(a, a_ptr, m0, L, cn);
     if (rc != TL_OK) return rc;
     TtvParams &P = L.P;

@@ -388,12 +388,19 @@ def components(args, wl=None):
         del g
         return statistics.median(ts)
 
-    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    flush_buf = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    flush_sink = torch.empty(1, dtype=torch.float32, device="cuda")
+
+    def flush_l2(r):
+        """Evict L2 by READING 512 MB (4x L2): clean lines, so the timed op
+        pays no write-back of the flush's own data (a write flush would leave
+        ~126 MB of dirty lines for the op to evict)."""
+        torch.sum(flush_buf, dim=0, keepdim=True, out=flush_sink)
 
     def cold(fn, reps=20, iters=5):
         """Device time of one launch with a cold L2: a CUDA graph of `reps`
-        x [512 MB write (4x L2), fn] minus a graph of `reps` x [the same
-        write], divided by `reps` -- no event or host launch overhead in the
+        x [512 MB read (4x L2), fn] minus a graph of `reps` x [the same
+        read], divided by `reps` -- no event or host launch overhead in the
         number (an event pair around a single eager launch adds ~6 us on
         this box: tools/experiments/red_probe.cu)."""
         s = torch.cuda.Stream()
@@ -408,7 +415,7 @@ def components(args, wl=None):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 for r in range(reps):
-                    flush_buf.fill_(float(r))
+                    flush_l2(r)
                     if with_fn:
                         fn()
             graphs.append(g)
@@ -507,7 +514,7 @@ def components(args, wl=None):
         C1 = tl.ttv(A, Vv, 5)
         t_ttm = cold(lambda: tl.ttm(C1, Bm5, 2))
         t_ttm_warm = med(lambda: tl.ttm(C1, Bm5, 2))
-        C2 = tl.ttm(C1, Bm5, 2)
+        C2 = tl.ttm(C1, Bm5, 2).copy()  # a copy: the standalone norm kernel, not ttm's fused value
         t_nrm = cold(lambda: C.frobenius_norm_device(C2))
         t_nrm_warm = med(lambda: C.frobenius_norm_device(C2))
 
@@ -518,7 +525,10 @@ def components(args, wl=None):
         # the whole config as the reference states it: ttv -> ttm -> norm of
         # the result, from a cold L2 (the intermediates then stay L2-resident
         # where they fit, as in any run)
-        t_chain = cold(chain)
+        t_chain = cold(chain)  # the norm comes from ttm's fused epilogue
+        os.environ["TL_FUSED_NORM"] = "0"
+        t_chain_unfused = cold(chain)  # ttm, then the norm kernel over its output
+        os.environ.pop("TL_FUSED_NORM")
         n5 = 96940800
         chain_bytes = 8 * (n5 + 9 + n5 // 9) + 8 * (10771200 + 528 + 5222400) + 8 * 5222400
         out[f"cfg5_seed{seed}"] = {
@@ -531,6 +541,7 @@ def components(args, wl=None):
             "norm_frac_hbm_cold": round(8 * 5222400 / (t_nrm * 1e-3) / 1e9 / peak, 3),
             "norm_us_l2warm": round(t_nrm_warm * 1e3, 1),
             "chain_us_cold": round(t_chain * 1e3, 1),
+            "chain_us_cold_norm_kernel": round(t_chain_unfused * 1e3, 1),
             "chain_frac_hbm": round(chain_bytes / (t_chain * 1e-3) / 1e9 / peak, 3),
         }
         del A, C1, C2

@@ -90,6 +90,17 @@ int tl_ttv(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_
 int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr,
            const tl_desc *c, void *c_ptr, int32_t mode, void *stream);
 
+/* tl_ttm, plus (when the chosen kernel supports it) the sum of squares of
+ * C computed in the same launch's epilogue: ssq_dev[0] = sum C^2,
+ * ssq_dev[1] = sqrt(sum C^2) = frobenius_norm(C) (contraction.py:462-464),
+ * deterministic, relative error < 1e-12.  *fused (host) is set to 1 when
+ * ssq_dev will be written, else 0 (then only C is produced).  ws: the
+ * tl_reduce_workspace_bytes() zeroed scratch.  No reference counterpart:
+ * this fuses the config-5 chain's norm into its ttm. */
+int tl_ttm_ssq(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr,
+               const tl_desc *c, void *c_ptr, int32_t mode, double *ssq_dev, void *ws,
+               size_t ws_bytes, int32_t *fused, void *stream);
+
 /* Workspace bytes needed by tl_inner / tl_frobenius_norm (fixed size). */
 size_t tl_reduce_workspace_bytes(void);
 

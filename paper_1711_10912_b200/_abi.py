@@ -29,6 +29,7 @@ EXPORTS = (
     "tl_init",
     "tl_ttv",
     "tl_ttm",
+    "tl_ttm_ssq",
     "tl_reduce_workspace_bytes",
     "tl_inner",
     "tl_inner_flat",
@@ -93,6 +94,8 @@ def load_library(path: str = LIB_PATH):
         L.tl_init.restype = ctypes.c_int
         L.tl_ttv.argtypes = [_dp, _vp, _dp, _vp, _dp, _vp, ctypes.c_int32, _vp]
         L.tl_ttm.argtypes = [_dp, _vp, _dp, _vp, _dp, _vp, ctypes.c_int32, _vp]
+        L.tl_ttm_ssq.argtypes = [_dp, _vp, _dp, _vp, _dp, _vp, ctypes.c_int32, _vp, _vp, ctypes.c_size_t,
+                                 ctypes.POINTER(ctypes.c_int32), _vp]
         L.tl_reduce_workspace_bytes.restype = ctypes.c_size_t
         L.tl_inner.argtypes = [_dp, _vp, _dp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_inner_flat.argtypes = [_dp, _vp, _dp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
@@ -112,7 +115,7 @@ def load_library(path: str = LIB_PATH):
         L.tl_times_vectors_workspace_bytes.argtypes = [_dp, ctypes.c_int32, i32p, _dp, ctypes.POINTER(ctypes.c_size_t)]
         L.tl_times_vectors.argtypes = [_dp, _vp, ctypes.c_int32, i32p, _dp, vpp, _dp, _vp, _vp, ctypes.c_size_t, _vp]
         L.tl_plan_describe.argtypes = [ctypes.c_int32, _dp, _dp, ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
-        for name in ("tl_ttv", "tl_ttm", "tl_inner", "tl_inner_flat", "tl_frobenius_norm", "tl_hopm_workspace_bytes", "tl_hopm",
+        for name in ("tl_ttv", "tl_ttm", "tl_ttm_ssq", "tl_inner", "tl_inner_flat", "tl_frobenius_norm", "tl_hopm_workspace_bytes", "tl_hopm",
                      "tl_hopm_graph_create", "tl_graph_launch", "tl_graph_destroy", "tl_copy", "tl_rank_one_compose",
                      "tl_residual", "tl_plan_describe", "tl_times_vectors_workspace_bytes", "tl_times_vectors"):
             getattr(L, name).restype = ctypes.c_int

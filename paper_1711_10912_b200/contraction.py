@@ -111,9 +111,26 @@ def ttm(a, bmat, mode: int) -> DenseTensor:
     m = mode - 1
     out = DenseTensor(A.shape[:m] + (Bm.shape[0],) + A.shape[m + 1:], dtype=A.dtype, device=A.device, fill_value=None)
     L = _abi.lib()
+    if A.dtype == torch.float64 and _fuse_norm():
+        # the small-J stream kernel also leaves ||C|| (its epilogue's sum of
+        # squares) for a following frobenius_norm(C)
+        ssq = torch.empty(2, dtype=torch.float64, device=A.device)
+        ws = _abi.reduce_workspace(A.device)
+        fused = ctypes.c_int32(0)
+        rc = L.tl_ttm_ssq(A.desc(), A.ptr(), Bm.desc(), Bm.ptr(), out.desc(), out.ptr(), int(mode), ssq.data_ptr(),
+                          ws.data_ptr(), ws.numel(), ctypes.byref(fused), _abi.stream_handle())
+        _abi.check(rc, "ttm")
+        if fused.value:
+            out._ssq = (ssq, out.buffer, out.buffer._version)
+        return out
     rc = L.tl_ttm(A.desc(), A.ptr(), Bm.desc(), Bm.ptr(), out.desc(), out.ptr(), int(mode), _abi.stream_handle())
     _abi.check(rc, "ttm")
     return out
+
+
+def _fuse_norm() -> bool:
+    """Fused ||C|| in ttm's epilogue (TL_FUSED_NORM=0 disables)."""
+    return os.environ.get("TL_FUSED_NORM", "1") != "0"
 
 
 def _reduce_result_buffer(dtype, device) -> torch.Tensor:
@@ -160,7 +177,13 @@ def inner_product_flat(a, b, init=0):
 
 
 def frobenius_norm_device(a) -> torch.Tensor:
+    """||a|| as a 1-element device tensor.  When the kernel that produced a's
+    current values already computed it (ttm's fused epilogue), that value is
+    returned without another pass over a."""
     A = _operand(a)
+    fused = A._fused_norm() if isinstance(a, DenseTensor) else None
+    if fused is not None:
+        return fused[1:2]
     if not _is_float(A.dtype):
         A = A.to(torch.float64)
     res = torch.empty(1, dtype=torch.float64, device=A.device)

@@ -27,7 +27,8 @@ int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
 int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                      int m0, cudaStream_t st);
 int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
-                       int m0, cudaStream_t st);
+                       int m0, cudaStream_t st, double *ssq_out = nullptr, void *ssq_ws = nullptr,
+                       int32_t *ssq_fused = nullptr);
 size_t reduce_workspace_bytes();
 int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const void *b_ptr, void *result,
                    bool do_sqrt, void *ws, size_t ws_bytes, cudaStream_t st, const void *init = nullptr);
@@ -200,8 +201,9 @@ int tl_ttv(const tl_desc *a, const void *a_ptr, const tl_desc *b, const void *b_
                        (cudaStream_t)stream, nullptr, false);
 }
 
-int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr, const tl_desc *c, void *c_ptr,
-           int32_t mode, void *stream) {
+static int ttm_dispatch(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr, const tl_desc *c,
+                        void *c_ptr, int32_t mode, void *stream, double *ssq_out, void *ssq_ws, int32_t *ssq_fused) {
+    if (ssq_fused != nullptr) *ssq_fused = 0;
     if (!check_desc(a, "ttm A") || !check_desc(bmat, "ttm matrix") || !check_desc(c, "ttm C")) return TL_EINVAL;
     const int p = a->order;
     if (p < 2) {
@@ -245,7 +247,7 @@ int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void 
     const bool few_rows = bmat->extent[0] <= 32;
     const bool fp = a->dtype == TL_F64 || a->dtype == TL_F32;
     if (few_rows || !fp) {
-        int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+        int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st, ssq_out, ssq_ws, ssq_fused);
         if (rc != TL_EUNSUPPORTED) return rc;
     }
     if (fp) {
@@ -257,6 +259,20 @@ int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void 
         }
     }
     return ttm_simt_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+}
+
+int tl_ttm(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr, const tl_desc *c, void *c_ptr,
+           int32_t mode, void *stream) {
+    return ttm_dispatch(a, a_ptr, bmat, b_ptr, c, c_ptr, mode, stream, nullptr, nullptr, nullptr);
+}
+
+int tl_ttm_ssq(const tl_desc *a, const void *a_ptr, const tl_desc *bmat, const void *b_ptr, const tl_desc *c,
+               void *c_ptr, int32_t mode, double *ssq_dev, void *ws, size_t ws_bytes, int32_t *fused, void *stream) {
+    if (ssq_dev != nullptr && (ws == nullptr || ws_bytes < reduce_workspace_bytes())) {
+        set_error("ttm: workspace of %zu bytes required", reduce_workspace_bytes());
+        return TL_EWORKSPACE;
+    }
+    return ttm_dispatch(a, a_ptr, bmat, b_ptr, c, c_ptr, mode, stream, ssq_dev, ws, fused);
 }
 
 size_t tl_reduce_workspace_bytes(void) { return reduce_workspace_bytes(); }

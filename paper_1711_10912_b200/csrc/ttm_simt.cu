@@ -39,6 +39,11 @@ struct TtmSimtParams {
     // index ranges past 2^32 (the one-thread-per-output kernel only)
     int32_t big;
     DigitMap64 in_map64, out_map64;
+    // optional fused sum of squares of C (stream kernel): per-CTA partials,
+    // last-CTA ticket, ssq_out = {sum C^2, sqrt(sum C^2)}
+    double *ssq_out;
+    double *ssq_partials;
+    unsigned int *ssq_ticket;
 };
 
 template <class T, class TC>
@@ -463,7 +468,59 @@ constexpr int kStreamMaxSlots = 48;
 constexpr size_t kStreamSmemBudget = 220 * 1024;  // one CTA per SM (227 KB max)
 constexpr int kStreamMaxWarps = 8;
 
-template <int MT, int NT>
+// Fused sum of squares of C for frobenius_norm(ttm(...)) (the config-5
+// chain ttv -> ttm -> norm): lane sums (FMA, <= kSsqChain terms each) ->
+// fixed-order warp tree -> warps 0..NW-1 in order (added by the CTA's last
+// consumer warp to finish) -> CTA partials 0..grid-1 in a fixed order (the
+// last CTA).  Every level has a fixed order, so the result is deterministic;
+// relative error <= (chain + 5 + log2 NW + grid) * 2^-53 < 1e-12.
+constexpr int64_t kSsqChain = 4096;
+
+struct SsqShared {
+    double wpart[kStreamMaxWarps];
+    unsigned int wdone;
+    int cta_last;
+};
+
+__device__ __noinline__ void stream_ssq_combine(const TtmSimtParams &P, double ssq, int warp, int NW, SsqShared &sh) {
+    double *wpart = sh.wpart;
+    unsigned int &wdone = sh.wdone;
+    int &cta_last = sh.cta_last;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) ssq += __shfl_down_sync(0xffffffffu, ssq, d);
+    int last_warp = 0;
+    if (lane == 0) {
+        wpart[warp] = ssq;
+        __threadfence_block();
+        last_warp = atomicAdd(&wdone, 1u) == (unsigned)NW - 1;
+    }
+    last_warp = __shfl_sync(0xffffffffu, last_warp, 0);
+    if (!last_warp) return;
+    __threadfence_block();
+    if (lane == 0) {
+        double cta = 0.0;
+        for (int w = 0; w < NW; ++w) cta += *(volatile double *)&wpart[w];
+        P.ssq_partials[blockIdx.x] = cta;
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(P.ssq_ticket) : "memory");
+        cta_last = prev == gridDim.x - 1;
+    }
+    __syncwarp();
+    if (!*(volatile int *)&cta_last) return;
+    // the last CTA: partials lane-strided in index order, then a fixed tree
+    double v = 0.0;
+    for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(P.ssq_partials + i);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    if (lane == 0) {
+        P.ssq_out[0] = v;
+        P.ssq_out[1] = sqrt(v);
+        *P.ssq_ticket = 0u;  // leave the workspace zeroed
+    }
+}
+
+template <int MT, int NT, bool SSQ = false>
 __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(const __grid_constant__ TtmSimtParams P,
                                                                               int SW) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -484,12 +541,14 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
         const int64_t j = e / ldb, k = e - j * ldb;
         bsm[e] = (j < J && k < K) ? ((const double *)P.bm)[j * P.bs0 + k * P.bs1] : 0.0;
     }
+    __shared__ SsqShared ssq_sh;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
         mbar_fence_init();
+        ssq_sh.wdone = 0u;
     }
     __syncthreads();
 
@@ -554,6 +613,7 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
     const int Kfull = Ki & ~3;  // k-steps with all four k in range
     const bool jfull = Ji == 16 * MT;
     int parity_out = 0;
+    double ssq4[4] = {0.0, 0.0, 0.0, 0.0};  // this lane's sums of squares of the outputs it stored (fused norm)
     int js = 0;         // j mod SW for this warp's j-th tile
     uint32_t jpar = 0;  // parity of fill j / SW
     for (int64_t q = warp; q < my_tiles; q += NW) {
@@ -609,7 +669,11 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
                     for (int mm = 0; mm < MT; ++mm)
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                            if (orow[nt][v] < P.R) ot[ooff[nt][v] + (mm * 16 + g + 8 * h) * Ii] = acc[mm][nt][2 * h + v];
+                            if (orow[nt][v] < P.R) {
+                                const double x = acc[mm][nt][2 * h + v];
+                                ot[ooff[nt][v] + (mm * 16 + g + 8 * h) * Ii] = x;
+                                if (SSQ) ssq4[(2 * h + v) & 3] = fma(x, x, ssq4[(2 * h + v) & 3]);
+                            }
         } else {
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
@@ -621,7 +685,11 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int j = mm * 16 + g + 8 * h;
-                            if (j < Ji) ot[ooff[nt][v] + j * Ii] = acc[mm][nt][2 * h + v];
+                            if (j < Ji) {
+                                const double x = acc[mm][nt][2 * h + v];
+                                ot[ooff[nt][v] + j * Ii] = x;
+                                if (SSQ) ssq4[(2 * h + v) & 3] = fma(x, x, ssq4[(2 * h + v) & 3]);
+                            }
                         }
                 }
         }
@@ -637,6 +705,7 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
         }
     }
     if (lane == 0) bulk_wait<0>();
+    if constexpr (SSQ) stream_ssq_combine(P, (ssq4[0] + ssq4[1]) + (ssq4[2] + ssq4[3]), warp, NW, ssq_sh);
 }
 
 static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
@@ -796,10 +865,18 @@ static bool staged_family_ok(const TtmSimtParams &P, int32_t dtype) {
              P.O > 0xffffffffll);
 }
 
+constexpr int kMaxSsqPartials = 148 * 8;  // the reduce workspace's partial slots
+
 int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
-                       int m0, cudaStream_t st) {
+                       int m0, cudaStream_t st, double *ssq_out, void *ssq_ws, int32_t *ssq_fused) {
+    if (ssq_fused != nullptr) *ssq_fused = 0;
     TtmSimtParams P{};
     if (!build_params(a, a_ptr, bm, b_ptr, c_ptr, m0, P)) return TL_EUNSUPPORTED;
+    if (ssq_out != nullptr && ssq_ws != nullptr) {
+        P.ssq_out = ssq_out;
+        P.ssq_partials = (double *)ssq_ws;
+        P.ssq_ticket = (unsigned int *)((unsigned char *)ssq_ws + (size_t)kMaxSsqPartials * 2 * sizeof(double));
+    }
     const int64_t s = (int64_t)dtype_size(a.dtype);
     const int64_t KI = P.K * P.I;
     if (P.O * P.I == 0) return TL_OK;
@@ -825,6 +902,30 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
             kern<<<(unsigned)grid, threads, smem, st>>>(P, sw);
             return cuda_status(cudaGetLastError(), "ttm stream launch");
         };
+        // fused sum of squares (frobenius_norm of this output): when every
+        // lane's FMA chain stays <= kSsqChain terms
+        const int64_t lanes = grid * sp.nw * 32;
+        const bool ssq = P.ssq_out != nullptr && (P.O * P.J * P.I + lanes - 1) / lanes <= kSsqChain &&
+                         grid <= kMaxSsqPartials;
+        if (!ssq) P.ssq_out = nullptr;
+        if (ssq_fused != nullptr) *ssq_fused = ssq ? 1 : 0;
+        if (ssq && P.J <= 16) {
+            switch (sp.nt) {
+                case 1: return go(ttm_stream_kernel<1, 1, true>);
+                case 2: return go(ttm_stream_kernel<1, 2, true>);
+                case 3: return go(ttm_stream_kernel<1, 3, true>);
+                case 4: return go(ttm_stream_kernel<1, 4, true>);
+                default: return go(ttm_stream_kernel<1, 5, true>);
+            }
+        }
+        if (ssq) {
+            switch (sp.nt) {
+                case 1: return go(ttm_stream_kernel<2, 1, true>);
+                case 2: return go(ttm_stream_kernel<2, 2, true>);
+                case 3: return go(ttm_stream_kernel<2, 3, true>);
+                default: return go(ttm_stream_kernel<2, 4, true>);
+            }
+        }
         if (P.J <= 16) {
             switch (sp.nt) {
                 case 1: return go(ttm_stream_kernel<1, 1>);

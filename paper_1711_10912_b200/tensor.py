@@ -147,13 +147,19 @@ class DenseTensor:
     """Dense array with runtime order, extents, offsets and layout, stored
     on the GPU in memory-index order."""
 
-    __slots__ = ("meta", "buffer")
+    # _ssq: (device [sum C^2, ||C||], the buffer it describes, its version)
+    # when a kernel computed the Frobenius norm of this tensor's values as it
+    # produced them (ttm's fused epilogue); valid while the buffer is the
+    # same object at the same torch version (every in-place write through
+    # this API -- .data, item/element setters, fill, copy_ -- bumps it)
+    __slots__ = ("meta", "buffer", "_ssq")
 
     def __init__(self, shape, offsets=None, layout=None, fill_value=0, dtype=None, device=None):
         """Value-initialised like the reference (tensor.py:44-46).
         ``fill_value=None`` leaves the buffer uninitialised (contraction
         outputs, which the kernels overwrite completely)."""
         self.meta = TensorMeta(shape, offsets, layout)
+        self._ssq = None
         dt = as_dtype(dtype)
         dev = _device(device)
         if fill_value is None:
@@ -167,7 +173,16 @@ class DenseTensor:
         t = cls.__new__(cls)
         t.meta = meta
         t.buffer = buffer
+        t._ssq = None
         return t
+
+    def _fused_norm(self):
+        """The device [sum of squares, norm] a producing kernel left for this
+        exact buffer state, or None."""
+        f = getattr(self, "_ssq", None)
+        if f is None or f[1] is not self.buffer or f[2] != self.buffer._version:
+            return None
+        return f[0]
 
     @classmethod
     def from_memory(cls, shape, data, offsets=None, layout=None, dtype=None, device=None) -> "DenseTensor":

@@ -545,3 +545,39 @@ def test_times_vectors_chain_equals_launch_sequence(gpu, dtype, monkeypatch):
         monkeypatch.setenv("TL_TV_CHAIN", "0")
         want = m.times_vectors(A, vs, modes).numpy()
         assert got.tobytes() == want.tobytes(), (shape, modes)
+
+
+def test_ttm_fused_norm(gpu, monkeypatch):
+    """frobenius_norm of an unmodified small-J float64 ttm output comes from
+    the ttm's own epilogue (one pass fewer); it agrees with the standalone
+    norm kernel and the exact value, is deterministic, and is dropped as
+    soon as the output is modified."""
+    m = tl()
+    from tolerance import check_inner
+
+    rng = np.random.default_rng(11)
+    for shape, mode, J in (((3, 33, 5, 17, 2, 64), 2, 16), ((5, 37, 2001), 2, 7), ((40, 999), 1, 20),
+                           ((3, 10, 2), 2, 5), ((9, 300, 41), 2, 32)):
+        T = rng.standard_normal(shape)
+        M = rng.standard_normal((J, shape[mode - 1]))
+        A = m.DenseTensor.from_memory(shape, T.ravel(order="F"))
+        Bm = m.DenseTensor.from_memory(M.shape, M.ravel(order="F"))
+        C = m.ttm(A, Bm, mode)
+        c = C.numpy()
+        n_plain = m.frobenius_norm(C.copy())  # a copy carries no fused value: the norm kernel
+        n_fused = m.frobenius_norm(C)
+        exact = check_inner(n_fused ** 2, float(np.dot(c, c)), c, c, rtol=1e-12)  # vs exact sum of squares
+        assert exact <= 1e-12
+        assert abs(n_fused - n_plain) <= 1e-12 * n_plain
+        assert m.frobenius_norm(m.ttm(A, Bm, mode)) == n_fused  # deterministic
+        C.data[0] = C.data[0] + 1.0  # any write drops the fused value
+        assert C._fused_norm() is None
+        C2 = m.ttm(A, Bm, mode)
+        C2.fill(0.0)
+        assert m.frobenius_norm(C2) == 0.0
+    # float32 and the GETT path carry none
+    A32 = m.DenseTensor.from_memory((3, 33, 5), rng.standard_normal((3, 33, 5)).astype(np.float32).ravel(order="F"))
+    B32 = m.DenseTensor.from_memory((16, 33), rng.standard_normal((16, 33)).astype(np.float32).ravel(order="F"))
+    assert m.ttm(A32, B32, 2)._fused_norm() is None
+    monkeypatch.setenv("TL_FUSED_NORM", "0")
+    assert m.ttm(A, Bm, mode)._fused_norm() is None

@@ -55,8 +55,19 @@ def main(which):
             keep += [A5, V, Bm5, C1, C2]
             ops.append(lambda A5=A5, V=V: tl.ttv(A5, V, 5))
             ops.append(lambda C1=C1, Bm5=Bm5: tl.ttm(C1, Bm5, 2))
-            ops.append(lambda C2=C2: C.frobenius_norm_device(C2))
+            C2n = C2.copy()  # no fused value: the standalone norm kernel
+            keep.append(C2n)
+            ops.append(lambda C2n=C2n: C.frobenius_norm_device(C2n))
             del T
+    if "copy" in which:
+        # relayout / transpose kernels on the config-2 tensor (first -> last,
+        # first -> seeded permutation, first -> (2,1,3,4))
+        T, _, _ = W.cfg2()
+        Af = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, (1, 2, 3, 4)))
+        keep += [Af]
+        for tau in ((4, 3, 2, 1), (3, 1, 2, 4), (2, 1, 3, 4)):
+            ops.append(lambda tau=tau: tl.transpose(Af, tau))
+        del T
     if "cfg4" in which:
         T, _ = W.cfg4()
         A4 = tl.DenseTensor.from_memory(T.shape, W.layout_buffer(T, (1, 2, 3)))

@@ -512,8 +512,10 @@ def components(args, wl=None):
         Bm5 = tl.DenseTensor.from_memory(M.shape, W.layout_buffer(M, (1, 2)))
         t_ttv = med(lambda: tl.ttv(A, Vv, 5))
         C1 = tl.ttv(A, Vv, 5)
+        os.environ["TL_FUSED_NORM"] = "0"  # the ttm alone (no fused norm epilogue)
         t_ttm = cold(lambda: tl.ttm(C1, Bm5, 2))
         t_ttm_warm = med(lambda: tl.ttm(C1, Bm5, 2))
+        os.environ.pop("TL_FUSED_NORM")
         C2 = tl.ttm(C1, Bm5, 2).copy()  # a copy: the standalone norm kernel, not ttm's fused value
         t_nrm = cold(lambda: C.frobenius_norm_device(C2))
         t_nrm_warm = med(lambda: C.frobenius_norm_device(C2))

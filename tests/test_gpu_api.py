@@ -3,6 +3,7 @@ regime, all ttm paths, the container API (relayout/assign/equality/
 interchange), error behaviour, allocation discipline, CUDA-graph capture,
 and full-size config-3 ttm checked on every output."""
 
+import json
 import os
 import random
 

@@ -561,19 +561,24 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
             int w = 0, js = 0;
             uint32_t jpar = 0;  // parity of fill j / SW
             bool wrapped = false;  // j >= SW: the slot has a previous tile
-            for (int64_t q = 0; q < my_tiles; ++q) {
+            // tile q starts at row o0 = (blockIdx.x + q * grid) * R: stepped, not recomputed
+            const int64_t tile_bytes = (int64_t)P.R * KI * 8;
+            const int64_t step_bytes = (int64_t)gridDim.x * tile_bytes;
+            const unsigned char *src = (const unsigned char *)P.a + (int64_t)blockIdx.x * tile_bytes;
+            int64_t o0 = (int64_t)blockIdx.x * P.R;
+            const int64_t o_step = (int64_t)gridDim.x * P.R;
+            for (int64_t q = 0; q < my_tiles; ++q, src += step_bytes, o0 += o_step) {
                 const int s = w * SW + js;
                 if (wrapped) mbar_wait_parity(&empty_bar[s], jpar ^ 1u);
-                const int64_t o0 = ((int64_t)blockIdx.x + q * gridDim.x) * P.R;
-                const int64_t rows = P.O - o0 < P.R ? P.O - o0 : P.R;
-                const uint32_t bytes = (uint32_t)(rows * KI * 8);
+                const uint32_t bytes = (P.O - o0 < P.R) ? (uint32_t)((P.O - o0) * KI * 8) : (uint32_t)tile_bytes;
                 const uint32_t b16 = bytes & ~15u;
                 unsigned char *dst = slots + s * slot_bytes;
-                const unsigned char *src = (const unsigned char *)((const double *)P.a + o0 * KI);
                 // an 8-byte tail (last tile, odd R*K*I) is copied here; the
                 // arrive below releases it to the consumer
-                if (bytes != b16) *(double *)(dst + b16) = *(const double *)(src + b16);
-                fence_proxy_async_smem();
+                if (bytes != b16) {
+                    *(double *)(dst + b16) = *(const double *)(src + b16);
+                    fence_proxy_async_smem();
+                }
                 mbar_arrive_expect_tx(&full_bar[s], b16);
                 if (b16) bulk_g2s(dst, src, b16, &full_bar[s]);
                 if (++w == NW) {

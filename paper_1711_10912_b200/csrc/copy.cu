@@ -25,6 +25,9 @@ struct CopyParams {
     int64_t nX, nY, n_rest, a_sX, a_sY, c_sY, tiles_x, tiles_y;
     DigitMap rest_a, rest_c;
     DigitMap64 amap64, cmap64;  // past 2^32 elements: the generic 64-bit copy
+    // rows: runs of row_len elements contiguous in both (16-byte vectors)
+    int64_t row_len, n_rows, nvec;
+    FastDiv vpr_div;  // vectors per row
 };
 
 template <class T> __global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyParams P) {
@@ -41,6 +44,37 @@ template <class T> __global__ void __launch_bounds__(256) copy64_kernel(const __
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P.n; q += stride)
         c[P.cmap64.map((uint64_t)q)] = a[P.amap64.map((uint64_t)q)];
+}
+
+// Source and destination share their fastest (merged) digit: copy whole
+// 16-byte vectors of each row; the row offsets come from the digit maps of
+// the row index, evaluated once per vector (not once per element).
+template <class T> __global__ void __launch_bounds__(256) copy_rows_kernel(const __grid_constant__ CopyParams P) {
+    constexpr int V = 16 / sizeof(T);
+    const T *a = (const T *)P.a;
+    T *c = (T *)P.c;
+    constexpr int U = 4;  // vectors in flight per thread
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + (U - 1) * stride < P.nvec; q += U * stride) {
+        uint4 x[U];
+        int64_t co[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t row, v;
+            P.vpr_div.divmod((uint32_t)(q + u * stride), row, v);
+            co[u] = P.cmap.map(row) + (int64_t)v * V;
+            x[u] = __ldcs((const uint4 *)(a + P.amap.map(row) + (int64_t)v * V));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) *(uint4 *)(c + co[u]) = x[u];
+    }
+    for (; q < P.nvec; q += stride) {
+        uint32_t row, v;
+        P.vpr_div.divmod((uint32_t)q, row, v);
+        const int64_t ao = P.amap.map(row) + (int64_t)v * V, co = P.cmap.map(row) + (int64_t)v * V;
+        *(uint4 *)(c + co) = __ldcs((const uint4 *)(a + ao));
+    }
 }
 
 template <class T> __global__ void __launch_bounds__(256) copy_tiled_kernel(const __grid_constant__ CopyParams P) {
@@ -125,6 +159,8 @@ template <class T> static cudaError_t launch_copy(const CopyParams &P, int kind,
         copy_tiled_kernel<T><<<grid, 256, 0, st>>>(P);
     else if (kind == 3)
         copy64_kernel<T><<<grid, 256, 0, st>>>(P);
+    else if (kind == 4)
+        copy_rows_kernel<T><<<grid, 256, 0, st>>>(P);
     else
         copy_kernel<T><<<grid, 256, 0, st>>>(P);
     return cudaGetLastError();
@@ -201,7 +237,11 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
             kind = 2;
             P.tiles_x = P.nX / kCT;
             P.tiles_y = P.nY / kCT;
-            grid = std::min<int64_t>(P.tiles_x * P.tiles_y * P.n_rest, (int64_t)di.num_sms * 4);
+            static const int64_t per_sm = [] {
+                const char *e = getenv("TL_COPY_CTAS_PER_SM");
+                return (int64_t)(e ? atoi(e) : 4);
+            }();
+            grid = std::min<int64_t>(P.tiles_x * P.tiles_y * P.n_rest, (int64_t)di.num_sms * per_sm);
         } else {
             P.tiles_x = (P.nX + 31) / 32;
             P.tiles_y = (P.nY + 31) / 32;
@@ -221,7 +261,21 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
             }
         }
         grid = std::min<int64_t>((P.n + 255) / 256, (int64_t)di.num_sms * 16);
-        if (P.n > kIdx32) {
+        const int64_t V = 16 / (int64_t)s;
+        bool rows = P.n <= kIdx32 && !la.empty() && la[0].second == 1 && lc[0].second == 1 && la[0].first % V == 0 &&
+                    (uintptr_t)P.a % 16 == 0 && (uintptr_t)P.c % 16 == 0;
+        for (size_t d = 1; rows && d < la.size(); ++d) rows = la[d].second % V == 0 && lc[d].second % V == 0;
+        if (rows) {
+            kind = 4;  // whole 16-byte vectors along the shared fastest digit
+            P.row_len = la[0].first;
+            P.n_rows = P.n / P.row_len;
+            P.nvec = P.n / V;
+            P.vpr_div.init((uint32_t)(P.row_len / V));
+            DigitList ra(la.begin() + 1, la.end()), rc(lc.begin() + 1, lc.end());
+            build_map(ra, P.amap);
+            build_map(rc, P.cmap);
+            grid = std::min<int64_t>((P.nvec + 255) / 256, (int64_t)di.num_sms * 8);
+        } else if (P.n > kIdx32) {
             kind = 3;  // 2^32+ elements: 64-bit digit maps
             build_map64(la, P.amap64);
             build_map64(lc, P.cmap64);

@@ -197,3 +197,22 @@ def test_ttt_large_vs_numpy(gpu, case):
     got = C.numpy().reshape(C.shape, order="F")
     assert got.shape == want.shape
     assert np.all(np.abs(got - want) <= RTOL64 * bound + 1e-300)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64", "int64"])
+def test_transpose_shared_fastest_dim_rows(gpu, dtype):
+    """Relayouts whose source and destination share the fastest dimension
+    copy whole 16-byte vectors per row (copy_rows_kernel): exact, including
+    rows that are not a multiple of the vector width (element path)."""
+    m = tl()
+    rng = np.random.default_rng(5)
+    for shape, tau in (((16, 5, 7, 3), (1, 3, 2, 4)), ((8, 33, 9), (1, 3, 2)), ((6, 4, 5), (1, 3, 2)),
+                       ((128, 3, 2, 5), (1, 4, 3, 2))):
+        T = rng.integers(-9, 9, size=shape) if dtype == "int64" else rng.standard_normal(shape).astype(dtype)
+        A = m.DenseTensor.from_memory(shape, T.ravel(order="F"))
+        got = m.transpose(A, tau).numpy()
+        want = np.transpose(T, [t - 1 for t in tau]).ravel(order="F")
+        assert got.tobytes() == want.astype(got.dtype).tobytes(), (shape, tau)
+        B = A.copy()
+        B.relayout(tau)
+        assert m.tensors_equal(A, B)

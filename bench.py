@@ -482,6 +482,15 @@ def components(args, wl=None):
     out["cfg3_ttm_tflops"] = tf
     out["cfg3_ttm_tflops_min"] = min(tf.values())
     out["cfg3_ttm_frac_fp64_peak_min"] = round(min(tf.values()) / FP64_PEAK_TFLOPS, 3)
+    # the same contraction as a general ttt (reduce_ttm_to_ttt: A's mode 2 with
+    # B's columns): two device relayouts + the GETT (contraction.py:337-369)
+    A1 = tl.DenseTensor.from_memory(A_.shape, W.layout_buffer(A_, (1, 2, 3)))
+    spec = tl.reduce_ttm_to_ttt(3, 2)
+    ms = med_eager(lambda: tl.ttt(A1, Bm, spec), iters=3, warm=1)
+    out["cfg3_ttt_q2_ms"] = round(ms, 3)
+    out["cfg3_ttt_q2_tflops"] = round(2 * 512 ** 3 * 384 / (ms * 1e-3) / 1e12, 2)
+    del A1
+    torch.cuda.empty_cache()
     # the same shape in float32 storage (widened onto the FP64 tensor cores;
     # an extension: the reference has no float32)
     A32 = tl.DenseTensor.from_memory(A_.shape, W.layout_buffer(A_, (1, 2, 3)).astype(np.float32))

@@ -34,6 +34,7 @@ def main(which):
                 ops.append(lambda A=As[n], m=m: tl.ttv(A, vs[m - 1], m))
         ops.append(lambda: C.frobenius_norm_device(As["first"]))
         ops.append(lambda: C.inner_product_device(As["first"], B))
+        ops.append(lambda: C.inner_product_device(As["first"], As["last"]))  # mixed layouts: dot_tiled
         del T, T2
     if "cfg3" in which:
         A_, B_ = W.cfg3()

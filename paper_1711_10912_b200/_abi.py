@@ -14,7 +14,8 @@ import threading
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libtlb200.so")
+# TL_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("TL_LIB") or os.path.join(_PKG, "_lib", "libtlb200.so")
 
 TL_MAX_ORDER = 16
 TL_F32, TL_F64, TL_I64 = 0, 1, 2

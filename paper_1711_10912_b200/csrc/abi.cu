@@ -21,7 +21,7 @@ namespace tl {
 struct FusedNorm;
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
                 int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
-                const FusedNorm *fn, bool pdl);
+                const FusedNorm *fn, bool pdl, int64_t keep_bytes = 0);
 int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                      int m0, cudaStream_t st);
 int ttm_dmma_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,

@@ -475,6 +475,7 @@ constexpr int kStreamMaxWarps = 8;
 // last CTA).  Every level has a fixed order, so the result is deterministic;
 // relative error <= (chain + 5 + log2 NW + grid) * 2^-53 < 1e-12.
 constexpr int64_t kSsqChain = 4096;
+constexpr int kSsqLoadsPerLane = 8;  // grids of up to 256 CTAs combine in one round trip
 
 struct SsqShared {
     double wpart[kStreamMaxWarps];
@@ -508,9 +509,20 @@ __device__ __noinline__ void stream_ssq_combine(const TtmSimtParams &P, double s
     }
     __syncwarp();
     if (!*(volatile int *)&cta_last) return;
-    // the last CTA: partials lane-strided in index order, then a fixed tree
+    // the last CTA: partials lane-strided in index order, then a fixed tree.
+    // All of a lane's loads are issued before the first add (one L2 round
+    // trip instead of one per 32 partials: the combine is the kernel's tail)
     double v = 0.0;
-    for (int i = lane; i < (int)gridDim.x; i += 32) v += __ldcg(P.ssq_partials + i);
+    const int G = (int)gridDim.x;
+    if (G <= 32 * kSsqLoadsPerLane) {
+        double x[kSsqLoadsPerLane];
+#pragma unroll
+        for (int q = 0; q < kSsqLoadsPerLane; ++q) x[q] = lane + 32 * q < G ? __ldcg(P.ssq_partials + lane + 32 * q) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kSsqLoadsPerLane; ++q) v += x[q];  // + 0.0 past the grid: exact (v >= 0)
+    } else {
+        for (int i = lane; i < G; i += 32) v += __ldcg(P.ssq_partials + i);
+    }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
     if (lane == 0) {

@@ -64,6 +64,12 @@ struct TtvParams {
     int32_t otab_d0;
     FastDiv otab_div;
     DigitMap out_hi;
+    // HOPM passes over A (strided regime, KEEP instantiation): k-rows
+    // k >= keep_k are loaded with the normal L2 policy, earlier rows
+    // evict-first, so the rows read last stay L2-resident for the next pass
+    // over A, and this pass's streaming fills do not evict the rows the
+    // previous pass left behind
+    int64_t keep_k;
 };
 
 // ------------------------------------------------------------- regime B
@@ -110,6 +116,13 @@ template <class TA, int VEC> struct RawLoad {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) v[j] = ld_stream(p + j);
     }
+    __device__ static void ld_hint(const TA *p, TA *v, uint64_t pol) {
+        static_assert(sizeof(TA) == 8, "L2-hinted loads: 64-bit elements");
+#pragma unroll
+        for (int j = 0; j < VEC; ++j)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
+                         : "=l"(*(uint64_t *)&v[j]) : "l"(p + j), "l"(pol));
+    }
 };
 template <> struct RawLoad<float, 4> {
     __device__ static void ld(const float *p, float *v) {
@@ -127,6 +140,10 @@ template <> struct RawLoad<double, 2> {
     __device__ static void ld(const double *p, double *v) {
         const double2 x = ld_stream_d2(p);
         v[0] = x.x; v[1] = x.y;
+    }
+    __device__ static void ld_hint(const double *p, double *v, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
     }
 };
 template <> struct RawLoad<int64_t, 2> {
@@ -164,7 +181,7 @@ __device__ __forceinline__ void store_outputs(const TtvParams &P, int64_t o, int
     }
 }
 
-template <class TA, class TC, int VEC, int U>
+template <class TA, class TC, int VEC, int U, bool KEEP = false>
 __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant__ TtvParams P) {
     using Acc = typename AccOf<TA>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -194,10 +211,21 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
         for (int j = 0; j < VEC; ++j) acc[j] = Acc(0);
 
         int64_t k = 0;
+        uint64_t pol_first = 0, pol_keep = 0;
+        if constexpr (KEEP) {
+            asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+            asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+        }
         for (; k + U <= K; k += U) {
             TA v[U][VEC];
+            if constexpr (KEEP) {
+                const uint64_t pol = (k + U > P.keep_k) ? pol_keep : pol_first;
 #pragma unroll
-            for (int u = 0; u < U; ++u) RawLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
+                for (int u = 0; u < U; ++u) RawLoad<TA, VEC>::ld_hint(pa + (k + u) * I, v[u], pol);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) RawLoad<TA, VEC>::ld(pa + (k + u) * I, v[u]);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const Acc bk = P.b_smem ? bs[k + u] : load_elem_as<Acc>(P.b, P.b_dtype, (k + u) * P.b_stride);
@@ -1208,6 +1236,9 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         if constexpr (sizeof(TA) == 4) {
             if (L.vec == 4) return go(ttv_strided_kernel<TA, TC, 4, U>);
         }
+        if constexpr (std::is_same<TA, double>::value) {
+            if (L.P.keep_k > 0) return L.vec == 2 ? go(ttv_strided_kernel<TA, TC, 2, U, true>) : go(ttv_strided_kernel<TA, TC, 1, U, true>);
+        }
         if (L.vec == 2) return go(ttv_strided_kernel<TA, TC, 2, U>);
         return go(ttv_strided_kernel<TA, TC, 1, U>);
     }
@@ -1549,7 +1580,7 @@ static int ttv_generic64_enqueue(const tl_desc &a, const void *a_ptr, const Cano
 // flag and binary64 outputs for float32 storage).
 int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t b_dtype, int64_t b_stride,
                 int32_t c_dtype, void *c_ptr, int m0, const int32_t *stop, cudaStream_t st,
-                const FusedNorm *fn, bool pdl) {
+                const FusedNorm *fn, bool pdl, int64_t keep_bytes) {
     TtvLaunch L{};
     Canon cn;
     if (canon_contraction(a, m0, 0, cn) && ttv_needs64(cn)) {
@@ -1564,6 +1595,11 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     TtvParams &P = L.P;
     if (P.O * P.I == 0) return TL_OK;
     L.pdl = pdl;
+    if (keep_bytes > 0 && L.regime == 0) {
+        // the last keep_bytes of A in this pass's k order stay in L2
+        const int64_t row = P.O * P.I * (int64_t)dtype_size(a.dtype);
+        P.keep_k = P.K - std::min<int64_t>(P.K, keep_bytes / row);
+    }
     P.b = b_ptr;
     P.c = c_ptr;
     P.stop = stop;

@@ -250,6 +250,7 @@ struct DeviceInfo {
     int device;
     int num_sms;
     int max_smem_optin;
+    int64_t l2_bytes;
 };
 // Cached per device on first use (no synchronisation; capture-safe after
 // the first call on a device).

@@ -24,6 +24,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <cstdio>
 #include <numeric>
 #include <type_traits>
@@ -64,12 +66,17 @@ struct TtvParams {
     int32_t otab_d0;
     FastDiv otab_div;
     DigitMap out_hi;
-    // HOPM passes over A (strided regime, KEEP instantiation): k-rows
-    // k >= keep_k are loaded with the normal L2 policy, earlier rows
-    // evict-first, so the rows read last stay L2-resident for the next pass
-    // over A, and this pass's streaming fills do not evict the rows the
-    // previous pass left behind
+    // L2 reuse between consecutive passes over one large tensor (HOPM's two
+    // passes per sweep; a ttv per mode of the same tensor): the part of A a
+    // pass reads LAST is loaded with the normal L2 policy and everything
+    // else evict-first, so it is still L2-resident when the next pass reads
+    // it, and the next pass's streaming fills evict each other instead of it.
+    // "Last" is k >= keep_k when the grid is one wave (all CTAs walk k
+    // together), CTAs >= keep_cta when it is several (later CTAs start later),
+    // tiles >= keep_tile for the persistent 2-D TMA rows kernel.
     int64_t keep_k;
+    int64_t keep_cta;
+    int64_t keep_tile;
 };
 
 // ------------------------------------------------------------- regime B
@@ -117,11 +124,15 @@ template <class TA, int VEC> struct RawLoad {
         for (int j = 0; j < VEC; ++j) v[j] = ld_stream(p + j);
     }
     __device__ static void ld_hint(const TA *p, TA *v, uint64_t pol) {
-        static_assert(sizeof(TA) == 8, "L2-hinted loads: 64-bit elements");
 #pragma unroll
-        for (int j = 0; j < VEC; ++j)
-            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
-                         : "=l"(*(uint64_t *)&v[j]) : "l"(p + j), "l"(pol));
+        for (int j = 0; j < VEC; ++j) {
+            if constexpr (sizeof(TA) == 8)
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
+                             : "=l"(*(uint64_t *)&v[j]) : "l"(p + j), "l"(pol));
+            else
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+                             : "=r"(*(uint32_t *)&v[j]) : "l"(p + j), "l"(pol));
+        }
     }
 };
 template <> struct RawLoad<float, 4> {
@@ -129,11 +140,19 @@ template <> struct RawLoad<float, 4> {
         const float4 x = ld_stream_f4(p);
         v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
     }
+    __device__ static void ld_hint(const float *p, float *v, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
+    }
 };
 template <> struct RawLoad<float, 2> {
     __device__ static void ld(const float *p, float *v) {
         const float2 x = ld_stream_f2(p);
         v[0] = x.x; v[1] = x.y;
+    }
+    __device__ static void ld_hint(const float *p, float *v, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(v[0]), "=f"(v[1]) : "l"(p), "l"(pol));
     }
 };
 template <> struct RawLoad<double, 2> {
@@ -150,6 +169,10 @@ template <> struct RawLoad<int64_t, 2> {
     __device__ static void ld(const int64_t *p, int64_t *v) {
         const longlong2 x = ld_stream_l2(p);
         v[0] = x.x; v[1] = x.y;
+    }
+    __device__ static void ld_hint(const int64_t *p, int64_t *v, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
+                     : "=l"(v[0]), "=l"(v[1]) : "l"(p), "l"(pol));
     }
 };
 
@@ -215,6 +238,7 @@ __global__ void __launch_bounds__(256) ttv_strided_kernel(const __grid_constant_
         if constexpr (KEEP) {
             asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
             asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+            if ((int64_t)blockIdx.x >= P.keep_cta) pol_first = pol_keep;
         }
         for (; k + U <= K; k += U) {
             TA v[U][VEC];
@@ -828,6 +852,15 @@ __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *m
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_hint(void *smem_dst, const CUtensorMap *map, int32_t c0, int32_t c1,
+                                                 uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 template <class TA, class TC>
 __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_constant__ TtvParams P,
                                                                  const __grid_constant__ CUtensorMap map) {
@@ -855,11 +888,21 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
     const int64_t nitems = my_tiles * nslab;
     int64_t p_tile = blockIdx.x;
     int p_slab = 0, p_stage = 0;
+    uint64_t pol_first = 0, pol_keep = 0;
+    const bool keep = P.keep_tile < ntiles;
+    if (keep && threadIdx.x == 0) {
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+        asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+    }
     auto issue_next = [&]() {
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&full_bar[p_stage], STAGE);
-            tma_load_2d(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * kRowsTmaR), &full_bar[p_stage]);
+            if (keep)
+                tma_load_2d_hint(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * kRowsTmaR), &full_bar[p_stage],
+                                 p_tile >= P.keep_tile ? pol_keep : pol_first);
+            else
+                tma_load_2d(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * kRowsTmaR), &full_bar[p_stage]);
         }
         if (++p_slab == nslab) {
             p_slab = 0;
@@ -928,6 +971,7 @@ struct TtvLaunch {
     bool vecread;
     bool bulk;
     bool pdl;  // programmatic dependent launch (HOPM chains)
+    int64_t keep_bytes;  // L2 reuse: bytes of A read last kept L2-resident (strided, 2-D TMA rows)
     bool small_cluster;  // small kernel + HOPM norm as one thread-block cluster
     bool rows_tma;     // regime S, I == 1, 2-D TMA tensor map
     int box_h;         // regime 4: warps per chain row (1 or 2)
@@ -1181,6 +1225,27 @@ static cudaError_t launch_rows_tma(const TtvLaunch &L, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kern, L.P, L.tmap);
 }
 
+// Resident CTAs per SM of a kernel configuration (cached: no per-launch query)
+static cudaError_t occupancy(const void *kern, int threads, size_t smem, int &per_sm) {
+    struct Entry {
+        const void *kern;
+        int threads;
+        size_t smem;
+        int per_sm;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry &c : cache)
+        if (c.kern == kern && c.threads == threads && c.smem == smem) {
+            per_sm = c.per_sm;
+            return cudaSuccess;
+        }
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (e == cudaSuccess) cache.push_back({kern, threads, smem, per_sm});
+    return e;
+}
+
 template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
     if (L.regime == 4) return launch_box<TA, TC>(L, st);
@@ -1229,18 +1294,32 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
             if (e != cudaSuccess) return e;
         }
+        if (L.regime == 0 && L.keep_bytes > 0) {
+            // what this pass reads last: its last k-rows (one wave) or its last CTAs
+            TtvLaunch K2 = L;
+            int per_sm = 0;
+            cudaError_t e = occupancy((const void *)kern, (int)L.block.x, L.smem, per_sm);
+            if (e != cudaSuccess) return e;
+            const int64_t resident = (int64_t)per_sm * device_info().num_sms;
+            const int64_t s = (int64_t)sizeof(TA);
+            if ((int64_t)L.grid.x <= resident) {
+                K2.P.keep_k = K2.P.K - std::min<int64_t>(K2.P.K, L.keep_bytes / (K2.P.O * K2.P.I * s));
+            } else {
+                const int64_t cta_bytes = (int64_t)L.block.x * L.vec * K2.P.K * s;
+                K2.P.keep_cta = (int64_t)L.grid.x - std::min<int64_t>(L.grid.x, L.keep_bytes / cta_bytes);
+            }
+            return launch_kernel(kern, K2, st);
+        }
         return launch_kernel(kern, L, st);
     };
     if (L.regime == 0) {
         constexpr int U = 8;
+        const bool keep = L.keep_bytes > 0;
         if constexpr (sizeof(TA) == 4) {
-            if (L.vec == 4) return go(ttv_strided_kernel<TA, TC, 4, U>);
+            if (L.vec == 4) return keep ? go(ttv_strided_kernel<TA, TC, 4, U, true>) : go(ttv_strided_kernel<TA, TC, 4, U>);
         }
-        if constexpr (std::is_same<TA, double>::value) {
-            if (L.P.keep_k > 0) return L.vec == 2 ? go(ttv_strided_kernel<TA, TC, 2, U, true>) : go(ttv_strided_kernel<TA, TC, 1, U, true>);
-        }
-        if (L.vec == 2) return go(ttv_strided_kernel<TA, TC, 2, U>);
-        return go(ttv_strided_kernel<TA, TC, 1, U>);
+        if (L.vec == 2) return keep ? go(ttv_strided_kernel<TA, TC, 2, U, true>) : go(ttv_strided_kernel<TA, TC, 2, U>);
+        return keep ? go(ttv_strided_kernel<TA, TC, 1, U, true>) : go(ttv_strided_kernel<TA, TC, 1, U>);
     }
     if (L.bulk) {
         if (L.vecread) return go(ttv_staged_kernel<TA, TC, 16, true, true>);
@@ -1595,11 +1674,9 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     TtvParams &P = L.P;
     if (P.O * P.I == 0) return TL_OK;
     L.pdl = pdl;
-    if (keep_bytes > 0 && L.regime == 0) {
-        // the last keep_bytes of A in this pass's k order stay in L2
-        const int64_t row = P.O * P.I * (int64_t)dtype_size(a.dtype);
-        P.keep_k = P.K - std::min<int64_t>(P.K, keep_bytes / row);
-    }
+    P.keep_k = P.K;  // nothing kept unless set below
+    P.keep_cta = INT64_MAX;
+    P.keep_tile = INT64_MAX;
     P.b = b_ptr;
     P.c = c_ptr;
     P.stop = stop;
@@ -1626,6 +1703,16 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
             B.stop = stop;
             B.b_stride = b_stride;
             B.b_dtype = b_dtype;
+        }
+    }
+    // L2 reuse only pays for tensors that stream (well past the L2 size)
+    const int64_t a_bytes = P.O * P.K * P.I * (int64_t)dtype_size(a.dtype);
+    if (keep_bytes > 0 && a_bytes >= 2 * (int64_t)device_info().l2_bytes && !L.small_cluster && L.regime != 4) {
+        if (L.regime == 0) {
+            L.keep_bytes = keep_bytes;  // split into keep_k / keep_cta at launch (needs the occupancy)
+        } else if (L.rows_tma) {
+            const int64_t ntiles = (P.O + kRowsTmaR - 1) / kRowsTmaR;
+            P.keep_tile = ntiles - std::min<int64_t>(ntiles, keep_bytes / (kRowsTmaR * P.K * (int64_t)dtype_size(a.dtype)));
         }
     }
     cudaError_t e;

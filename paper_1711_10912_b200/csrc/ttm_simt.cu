@@ -466,6 +466,8 @@ __global__ void __launch_bounds__(256) ttm_bulk_kernel(const __grid_constant__ T
 // Same per-element arithmetic as the other DMMA kernels (k-ordered FMA).
 constexpr int kStreamMaxSlots = 48;
 constexpr size_t kStreamSmemBudget = 220 * 1024;  // one CTA per SM (227 KB max)
+// per-CTA budget with c CTAs per SM (1 KB reserved per CTA, static smem)
+static size_t stream_budget(int c) { return c <= 1 ? kStreamSmemBudget : (228 * 1024) / (size_t)c - 4 * 1024; }
 constexpr int kStreamMaxWarps = 8;
 
 // Fused sum of squares of C for frobenius_norm(ttm(...)) (the config-5
@@ -549,10 +551,6 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
     const size_t otile = ((size_t)P.R * J * I * 8 + 15) & ~(size_t)15;
     unsigned char *outs = slots + (size_t)S * slot_bytes;
 
-    for (int64_t e = threadIdx.x; e < jpad * ldb; e += blockDim.x) {
-        const int64_t j = e / ldb, k = e - j * ldb;
-        bsm[e] = (j < J && k < K) ? ((const double *)P.bm)[j * P.bs0 + k * P.bs1] : 0.0;
-    }
     __shared__ SsqShared ssq_sh;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -563,6 +561,16 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
         ssq_sh.wdone = 0u;
     }
     __syncthreads();
+    // the producer starts streaming A at once; the consumer warps stage B
+    // meanwhile (its global loads' latency overlaps the first tiles') and
+    // meet at a named barrier of their own
+    if ((int)(threadIdx.x >> 5) < NW) {
+        for (int64_t e = threadIdx.x; e < jpad * ldb; e += NW * 32) {
+            const int64_t j = e / ldb, k = e - j * ldb;
+            bsm[e] = (j < J && k < K) ? ((const double *)P.bm)[j * P.bs0 + k * P.bs1] : 0.0;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    }
 
     const int64_t my_tiles = (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -758,7 +766,7 @@ static bool build_params(const tl_desc &a, const void *a_ptr, const tl_desc &bm,
 // Tuning knobs of the small-J kernels (environment, read once).
 struct SmallTtmKnobs {
     int64_t stage_kb = 28, bulk_kb = 14, stream_kb = 12;
-    int ntile = 4, bulk_nt = 2, bulk_st = 2, stream_nw = kStreamMaxWarps;
+    int ntile = 4, bulk_nt = 2, bulk_st = 2, stream_nw = kStreamMaxWarps, stream_cps = 1;
     bool force_simt = false;
 };
 static const SmallTtmKnobs &small_ttm_knobs() {
@@ -775,6 +783,7 @@ static const SmallTtmKnobs &small_ttm_knobs() {
         v.bulk_nt = (int)num("TL_TTM_BULK_NT", 2);
         v.bulk_st = (int)num("TL_TTM_BULK_ST", 2);  // measured: 2 stages (more CTAs per SM) beat 3-4
         v.stream_kb = num("TL_TTM_STREAM_KB", 12);  // tile target; 0 disables the stream kernel
+        v.stream_cps = (int)std::max<int64_t>(1, std::min<int64_t>(4, num("TL_TTM_STREAM_CPS", 1)));  // CTAs per SM
         v.stream_nw = (int)std::max<int64_t>(1, std::min<int64_t>(kStreamMaxWarps, num("TL_TTM_STREAM_NW", kStreamMaxWarps)));
         return v;
     }();
@@ -806,7 +815,7 @@ static bool plan_stream(const TtmSimtParams &P, StreamPlan &sp) {
         const int64_t pos = R * P.I;
         const double eff = (double)pos / (double)(8 * ((pos + 7) / 8));
         const size_t per_warp = 2 * (((size_t)R * P.J * P.I * 8 + 15) & ~(size_t)15) + 2 * (((size_t)R * KI * 8 + 15) & ~(size_t)15);
-        const bool fit = bb + (size_t)kn.stream_nw * per_warp <= kStreamSmemBudget;
+        const bool fit = bb + (size_t)kn.stream_nw * per_warp <= stream_budget(kn.stream_cps);
         const bool better = (fit != best_fit) ? fit : (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && R > bestR));
         if (bestR == 0 || better) {
             best_fit = fit;
@@ -821,8 +830,9 @@ static bool plan_stream(const TtmSimtParams &P, StreamPlan &sp) {
     // tiles; fewer warps when the smem budget demands it
     int nw = kn.stream_nw, sw = 0;
     for (; nw >= 2; --nw) {
-        if (bb + (size_t)nw * (2 * otile + 2 * slot_bytes) > kStreamSmemBudget) continue;
-        sw = (int)std::min<size_t>(kStreamMaxSlots / nw, (kStreamSmemBudget - bb - (size_t)nw * 2 * otile) / ((size_t)nw * slot_bytes));
+        const size_t budget = stream_budget(kn.stream_cps);
+        if (bb + (size_t)nw * (2 * otile + 2 * slot_bytes) > budget) continue;
+        sw = (int)std::min<size_t>(kStreamMaxSlots / nw, (budget - bb - (size_t)nw * 2 * otile) / ((size_t)nw * slot_bytes));
         break;
     }
     if (sw < 2) return false;
@@ -909,7 +919,7 @@ int ttm_staged_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, c
         P.ntiles = (P.O + sp.R - 1) / sp.R;
         P.I_div.init((uint32_t)P.I);
         const DeviceInfo &di = device_info();
-        const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms);
+        const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * kn.stream_cps);
         const int threads = 32 * (sp.nw + 1);
         const size_t smem = sp.smem;
         const int sw = sp.sw;

@@ -5,8 +5,10 @@
 set -u
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1
+if [ -n "${PARITY_CFG3:-}" ]; then
 TL_PARITY_REPORT=$PWD/gpurun_out/parity_report.jsonl timeout 1200 python -m pytest tests -m gpu -q -k cfg3_ttm_full_size \
     > gpurun_out/parity_cfg3.log 2>&1
+fi
 tail -1 gpurun_out/bench_full.log > gpurun_out/bench_line.json
 CMD="python bench.py --steps 2 --warmup 3 --no-components --no-cpu --no-e2e"
 timeout 300 $CMD > gpurun_out/bench_small.log 2>&1 && \
@@ -18,5 +20,6 @@ tools/ncu_box.sh prof_red "dot_" cfg2
 tools/ncu_box.sh prof_hopm "ttv_" cfg4
 tools/ncu_box.sh prof_cfg5 "ttv_|ttm_|dot_" cfg5
 tools/ncu_box.sh prof_copy "copy" copy
+tools/experiments/hopm_dram.sh
 rm -f gpurun_out/*.ncu-rep
 du -sh gpurun_out

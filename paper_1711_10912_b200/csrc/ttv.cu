@@ -74,9 +74,13 @@ struct TtvParams {
     // "Last" is k >= keep_k when the grid is one wave (all CTAs walk k
     // together), CTAs >= keep_cta when it is several (later CTAs start later),
     // tiles >= keep_tile for the persistent 2-D TMA rows kernel.
+    // l2_stream: the policy is on (else plain loads); the output always keeps
+    // the normal policy and is counted against the budget first, so a large
+    // ttv output (a short fold) stays L2-resident for its consumer.
     int64_t keep_k;
     int64_t keep_cta;
     int64_t keep_tile;
+    int32_t l2_stream;
 };
 
 // ------------------------------------------------------------- regime B
@@ -889,7 +893,7 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
     int64_t p_tile = blockIdx.x;
     int p_slab = 0, p_stage = 0;
     uint64_t pol_first = 0, pol_keep = 0;
-    const bool keep = P.keep_tile < ntiles;
+    const bool keep = P.l2_stream != 0;
     if (keep && threadIdx.x == 0) {
         asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
         asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
@@ -1294,7 +1298,7 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
             if (e != cudaSuccess) return e;
         }
-        if (L.regime == 0 && L.keep_bytes > 0) {
+        if (L.regime == 0 && L.P.l2_stream) {
             // what this pass reads last: its last k-rows (one wave) or its last CTAs
             TtvLaunch K2 = L;
             int per_sm = 0;
@@ -1314,7 +1318,7 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
     };
     if (L.regime == 0) {
         constexpr int U = 8;
-        const bool keep = L.keep_bytes > 0;
+        const bool keep = L.P.l2_stream != 0;
         if constexpr (sizeof(TA) == 4) {
             if (L.vec == 4) return keep ? go(ttv_strided_kernel<TA, TC, 4, U, true>) : go(ttv_strided_kernel<TA, TC, 4, U>);
         }
@@ -1677,6 +1681,7 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     P.keep_k = P.K;  // nothing kept unless set below
     P.keep_cta = INT64_MAX;
     P.keep_tile = INT64_MAX;
+    P.l2_stream = 0;
     P.b = b_ptr;
     P.c = c_ptr;
     P.stop = stop;
@@ -1708,11 +1713,17 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
     // L2 reuse only pays for tensors that stream (well past the L2 size)
     const int64_t a_bytes = P.O * P.K * P.I * (int64_t)dtype_size(a.dtype);
     if (keep_bytes > 0 && a_bytes >= 2 * (int64_t)device_info().l2_bytes && !L.small_cluster && L.regime != 4) {
+        // the output (normal policy) comes out of the budget first
+        const int64_t out_bytes = P.O * P.I * (int64_t)dtype_size(c_dtype);
+        const int64_t in_keep = std::max<int64_t>(0, keep_bytes - out_bytes);
+        const int64_t s = (int64_t)dtype_size(a.dtype);
         if (L.regime == 0) {
-            L.keep_bytes = keep_bytes;  // split into keep_k / keep_cta at launch (needs the occupancy)
+            P.l2_stream = 1;
+            L.keep_bytes = in_keep;  // split into keep_k / keep_cta at launch (needs the occupancy)
         } else if (L.rows_tma) {
+            P.l2_stream = 1;
             const int64_t ntiles = (P.O + kRowsTmaR - 1) / kRowsTmaR;
-            P.keep_tile = ntiles - std::min<int64_t>(ntiles, keep_bytes / (kRowsTmaR * P.K * (int64_t)dtype_size(a.dtype)));
+            P.keep_tile = ntiles - std::min<int64_t>(ntiles, in_keep / (kRowsTmaR * P.K * s));
         }
     }
     cudaError_t e;

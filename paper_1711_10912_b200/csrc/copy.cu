@@ -9,6 +9,7 @@
 // destination's, a 32x32 shared-memory tile transposes so that both the
 // loads and the stores coalesce.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "plan.h"
@@ -49,11 +50,11 @@ template <class T> __global__ void __launch_bounds__(256) copy64_kernel(const __
 // Source and destination share their fastest (merged) digit: copy whole
 // 16-byte vectors of each row; the row offsets come from the digit maps of
 // the row index, evaluated once per vector (not once per element).
-template <class T> __global__ void __launch_bounds__(256) copy_rows_kernel(const __grid_constant__ CopyParams P) {
+template <class T, int U> __global__ void __launch_bounds__(256) copy_rows_kernel(const __grid_constant__ CopyParams P) {
     constexpr int V = 16 / sizeof(T);
     const T *a = (const T *)P.a;
     T *c = (T *)P.c;
-    constexpr int U = 4;  // vectors in flight per thread
+    // U vectors in flight per thread
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; q + (U - 1) * stride < P.nvec; q += U * stride) {
@@ -119,20 +120,32 @@ template <class T> __global__ void __launch_bounds__(256) copy_tiled_vec_kernel(
     T *c = (T *)P.c;
     const int64_t per_rest = P.tiles_x * P.tiles_y;
     const int64_t tiles = per_rest * P.n_rest;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    struct Origin {
+        int64_t x0, y0, ra, rc;
+    };
+    auto origin = [&](int64_t t) {
         const int64_t rest = t / per_rest;
         const int64_t txy = t - rest * per_rest;
         const int64_t ty = txy / P.tiles_x;
         const int64_t tx = txy - ty * P.tiles_x;
-        const int64_t x0 = tx * kCT, y0 = ty * kCT;
-        const int64_t ra = P.rest_a.map((uint32_t)rest), rc = P.rest_c.map((uint32_t)rest);
-        T v[NV][V];
+        return Origin{tx * kCT, ty * kCT, P.rest_a.map((uint32_t)rest), P.rest_c.map((uint32_t)rest)};
+    };
+    // the next tile's loads are in flight while this tile is transposed and
+    // stored (one tile of registers ahead; the loads are the long latency)
+    T v[NV][V];
+    auto load = [&](const Origin &o) {
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
             const int e = threadIdx.x + q * 256;
             const int row = e / VR, vc = (e % VR) * V;  // source row x = row, y = vc..
-            *(uint4 *)v[q] = __ldcs((const uint4 *)(a + ra + (x0 + row) * P.a_sX + y0 + vc));
+            *(uint4 *)v[q] = __ldcs((const uint4 *)(a + o.ra + (o.x0 + row) * P.a_sX + o.y0 + vc));
         }
+    };
+    int64_t t = blockIdx.x;
+    if (t >= tiles) return;
+    Origin cur = origin(t);
+    load(cur);
+    for (; t < tiles; t += gridDim.x) {
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
             const int e = threadIdx.x + q * 256;
@@ -141,14 +154,21 @@ template <class T> __global__ void __launch_bounds__(256) copy_tiled_vec_kernel(
             for (int cc = 0; cc < V; ++cc) ts[(vc + cc) * kCT + (row ^ swz(vc + cc))] = v[q][cc];
         }
         __syncthreads();
+        const int64_t tn = t + gridDim.x;
+        Origin nxt = cur;
+        if (tn < tiles) {
+            nxt = origin(tn);
+            load(nxt);
+        }
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
             const int e = threadIdx.x + q * 256;
             const int row = e / VR, vc = (e % VR) * V;  // destination row y = row, x = vc..
             const uint4 w = *(const uint4 *)(ts + row * kCT + (vc ^ swz(row)));
-            __stcs((uint4 *)(c + rc + (y0 + row) * P.c_sY + x0 + vc), w);
+            __stcs((uint4 *)(c + cur.rc + (cur.y0 + row) * P.c_sY + cur.x0 + vc), w);
         }
         __syncthreads();
+        cur = nxt;
     }
 }
 
@@ -159,8 +179,16 @@ template <class T> static cudaError_t launch_copy(const CopyParams &P, int kind,
         copy_tiled_kernel<T><<<grid, 256, 0, st>>>(P);
     else if (kind == 3)
         copy64_kernel<T><<<grid, 256, 0, st>>>(P);
-    else if (kind == 4)
-        copy_rows_kernel<T><<<grid, 256, 0, st>>>(P);
+    else if (kind == 4) {
+        static const int u = [] {
+            const char *e = getenv("TL_COPY_ROWS_U");
+            return e ? atoi(e) : 4;
+        }();
+        if (u >= 8)
+            copy_rows_kernel<T, 8><<<grid, 256, 0, st>>>(P);
+        else
+            copy_rows_kernel<T, 4><<<grid, 256, 0, st>>>(P);
+    }
     else
         copy_kernel<T><<<grid, 256, 0, st>>>(P);
     return cudaGetLastError();
@@ -274,7 +302,11 @@ int copy_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &c, void *c_
             DigitList ra(la.begin() + 1, la.end()), rc(lc.begin() + 1, lc.end());
             build_map(ra, P.amap);
             build_map(rc, P.cmap);
-            grid = std::min<int64_t>((P.nvec + 255) / 256, (int64_t)di.num_sms * 8);
+            static const int64_t rows_per_sm = [] {
+                const char *e = getenv("TL_COPY_ROWS_CTAS_PER_SM");
+                return (int64_t)(e ? atoi(e) : 8);
+            }();
+            grid = std::min<int64_t>((P.nvec + 255) / 256, (int64_t)di.num_sms * rows_per_sm);
         } else if (P.n > kIdx32) {
             kind = 3;  // 2^32+ elements: 64-bit digit maps
             build_map64(la, P.amap64);

@@ -452,13 +452,13 @@ def components(args, wl=None):
     # a6) and the layout conversions the e2e relies on (relayout/transpose)
     if wl is not None:
         Af, Al = wl.A["first"], wl.A["last"]
-        ms = med_eager(lambda: C.inner_product_device(Af, Al), iters=7)
+        ms = med(lambda: C.inner_product_device(Af, Al), iters=5, reps=5)
         out["cfg2_inner_first_x_last_us"] = round(ms * 1e3, 1)
         out["cfg2_inner_first_x_last_frac_hbm"] = round(INNER_BYTES / (ms * 1e-3) / 1e9 / peak, 3)
         relay = {}
         for name, tau in (("first_to_last", (4, 3, 2, 1)), ("first_to_perm3124", (3, 1, 2, 4)),
                           ("first_to_2134", (2, 1, 3, 4))):
-            ms = med_eager(lambda: tl.transpose(Af, tau), iters=7)
+            ms = med(lambda: tl.transpose(Af, tau), iters=5, reps=5)
             relay[name] = {"us": round(ms * 1e3, 1), "frac_hbm": round(2 * 4 * N4 / (ms * 1e-3) / 1e9 / peak, 3)}
         out["cfg2_transpose"] = relay
         torch.cuda.empty_cache()

@@ -670,7 +670,11 @@ __global__ void __launch_bounds__(32 * (kStreamMaxWarps + 1)) ttm_stream_kernel(
                 for (int nt = 0; nt < NT; ++nt) mma_16x8x4_s(acc[mm][nt], a0, a1, bf[nt]);
             }
         };
-#pragma unroll 4
+        // two m16 tiles x 4 n8 tiles keep 64 accumulator registers live:
+        // unrolling 4 k-steps there spilled (148 bytes; 124 with the fused
+        // norm's registers), 2 (1 with the fused norm) does not
+        constexpr int KU = (MT * NT > 6) ? (SSQ ? 1 : 2) : 4;
+#pragma unroll KU
         for (int k4 = 0; k4 < Kfull; k4 += 4) kstep(k4, true);
         if (Kfull < Ki) kstep(Kfull, Kfull + t < Ki);
         __syncwarp();

@@ -610,6 +610,192 @@ __global__ void __launch_bounds__(256) ttv_small_kernel(const __grid_constant__ 
     }
 }
 
+// ------------------------------------------------------------- long folds, few outputs
+// Few outputs with a long fold (O*I/VEC threads too few to keep HBM busy
+// with a handful of loads in flight each): every thread keeps the next
+// NG*8 k-rows of ITS OWN fibre in flight through a private shared-memory
+// ring filled by cp.async (no data shared between threads, so no CTA
+// barriers: cp.async.wait_group is per thread), and folds them in k order
+// (bit-exact).  COLS: VEC consecutive i of one o (A[o][k][i0..], the strided
+// regime's fibres); ROWS (I == 1): one o, 16-byte chunks along its
+// contiguous row.  The sequential fold itself (8.2-cycle DADD chain) is the
+// floor once the ring hides the memory latency.
+constexpr int kDeepGroup = 8;
+
+template <class TA, class TC, int VEC, bool ROWS, int NG>
+__global__ void __launch_bounds__(64) ttv_deep_kernel(const __grid_constant__ TtvParams P) {
+    using Acc = typename AccOf<TA>::type;
+    constexpr int D = NG * kDeepGroup;  // pieces in flight per thread
+    constexpr int CH = ROWS ? (VEC > 1 ? 16 / (int)sizeof(TA) : 1) : VEC;  // A elements per piece
+    constexpr int CB = ROWS ? CH : 1;                                        // b elements per piece
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    if (stop_requested(P.stop)) return;
+    // private rings (A pieces, then the b values they fold with, b in A's
+    // type: the planner takes this kernel only when b's dtype is A's),
+    // pitched one 16-byte slot apart so a warp's same-slot accesses spread
+    // over all banks (4 wavefronts for 32 x 16 B, not 32)
+    constexpr int PITCH = D * (CH + CB) + 16 / (int)sizeof(TA);
+    TA *ring = (TA *)smem_raw + (size_t)threadIdx.x * PITCH;
+    TA *bring = ring + D * CH;
+    const int64_t K = P.K, I = P.I;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = ROWS ? P.O : P.O * (I / VEC);
+    if (gid >= nthr) return;
+    const int64_t og = ROWS ? gid : gid / (I / VEC);
+    const int64_t i0 = ROWS ? 0 : (gid - og * (I / VEC)) * VEC;
+    const TA *pa = (const TA *)P.a + (og * K) * I + i0;
+    const TA *pb = (const TA *)P.b;
+    // piece p: COLS = k-row p (VEC elements at pa + p*I), ROWS = chunk p (CH elements at pa + p*CH)
+    const int64_t npieces = ROWS ? (K + CH - 1) / CH : K;
+    auto issue = [&](int64_t p) {
+        if (p < npieces) {
+            const int slot = (int)(p % D);
+            TA *dst = ring + slot * CH;
+            TA *bdst = bring + slot * CB;
+            if constexpr (ROWS) {
+                if ((p + 1) * CH <= K) {
+                    cp_async<CH * sizeof(TA)>(dst, pa + p * CH);
+#pragma unroll
+                    for (int e = 0; e < CB; ++e) cp_async<sizeof(TA)>(bdst + e, pb + (p * CH + e) * P.b_stride);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < CH; ++e)
+                        if (p * CH + e < K) {
+                            cp_async<sizeof(TA)>(dst + e, pa + p * CH + e);
+                            cp_async<sizeof(TA)>(bdst + e, pb + (p * CH + e) * P.b_stride);
+                        }
+                }
+            } else {
+                cp_async<VEC * sizeof(TA)>(dst, pa + p * I);
+                cp_async<sizeof(TA)>(bdst, pb + p * P.b_stride);
+            }
+        }
+    };
+#pragma unroll 1
+    for (int g = 0; g < NG; ++g) {
+#pragma unroll
+        for (int r = 0; r < kDeepGroup; ++r) issue((int64_t)g * kDeepGroup + r);
+        cp_async_commit();
+    }
+    Acc acc[ROWS ? 1 : VEC];
+#pragma unroll
+    for (int j = 0; j < (ROWS ? 1 : VEC); ++j) acc[j] = Acc(0);
+    for (int64_t p0 = 0; p0 < npieces; p0 += kDeepGroup) {
+        cp_async_wait<NG - 1>();  // the oldest group has landed
+        const int s0 = (int)(p0 % D);
+        // the group's values first (independent shared loads), then the chain
+        TA av[kDeepGroup][CH], bv[kDeepGroup][CB];
+#pragma unroll
+        for (int r = 0; r < kDeepGroup; ++r) {
+#pragma unroll
+            for (int e = 0; e < CH; ++e) av[r][e] = ring[(s0 + r) * CH + e];
+#pragma unroll
+            for (int e = 0; e < CB; ++e) bv[r][e] = bring[(s0 + r) * CB + e];
+        }
+#pragma unroll
+        for (int r = 0; r < kDeepGroup; ++r) {
+            const int64_t p = p0 + r;
+            if (p < npieces) {
+                if constexpr (ROWS) {
+#pragma unroll
+                    for (int e = 0; e < CH; ++e)
+                        if (p * CH + e < K) acc[0] = fold_step(acc[0], (Acc)av[r][e], (Acc)bv[r][e]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) acc[j] = fold_step(acc[j], (Acc)av[r][j], (Acc)bv[r][0]);
+                }
+            }
+        }
+        // refill the slots just consumed (after the reads above: same thread)
+#pragma unroll
+        for (int r = 0; r < kDeepGroup; ++r) issue(p0 + D + r);
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+    if constexpr (ROWS) {
+        TC *c = (TC *)P.c;
+        c[P.ident ? og : P.out_map.map((uint32_t)og)] = narrow<TC>(acc[0]);
+    } else {
+        store_outputs<TC, VEC>(P, og, i0, acc);
+    }
+    pdl_release();
+}
+
+// ------------------------------------------------------------- short folds
+// K <= kShortK over a large tensor: the output is a sizeable fraction of the
+// input (N/K), so the contraction is an elementwise stream.  Each thread
+// produces QV consecutive outputs of the canonical order q = o*I + i, folding
+// k in order (bit-exact), into C in that order (ident) or through the digit
+// maps when C's fastest canonical digit is contiguous (runs of >= 32; other
+// permuted outputs stay on the tiled kernels: a temporary + transpose
+// measured slower there).  The loads go through L1: neighbouring threads and
+// k's share sectors.
+constexpr int kShortK = 16;
+
+template <class TA, class TC, int QV>
+__global__ void __launch_bounds__(256) ttv_short_kernel(const __grid_constant__ TtvParams P, TC *out) {
+    // out == nullptr: permuted C written through the digit maps (its fastest
+    // canonical digit is C-contiguous: runs of >= 32 outputs)
+    using Acc = typename AccOf<TA>::type;
+    __shared__ Acc bs[kShortK];
+    pdl_wait();
+    if (stop_requested(P.stop)) return;
+    const int K = (int)P.K;
+    if (threadIdx.x < K) bs[threadIdx.x] = load_elem_as<Acc>(P.b, P.b_dtype, threadIdx.x * P.b_stride);
+    __syncthreads();
+    const TA *a = (const TA *)P.a;
+    const int64_t nq = P.O * P.I;
+    const int64_t KI = P.K * P.I;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * QV;
+    for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * QV; q0 < nq; q0 += step) {
+        Acc acc[QV];
+        uint32_t o, i;
+        P.I_div.divmod((uint32_t)q0, o, i);  // q0 < 2^32 (planned)
+#pragma unroll
+        for (int j = 0; j < QV; ++j) {
+            acc[j] = Acc(0);
+            if (q0 + j < nq) {
+                const TA *pa = a + (int64_t)o * KI + i;
+#pragma unroll 4
+                for (int k = 0; k < K; ++k) acc[j] = fold_step(acc[j], (Acc)__ldg(pa + (int64_t)k * P.I), bs[k]);
+            }
+            if (++i == (uint32_t)P.I) {
+                i = 0;
+                ++o;
+            }
+        }
+        if (P.ident == 0) {
+            uint32_t o2, i2;
+            P.I_div.divmod((uint32_t)q0, o2, i2);
+#pragma unroll
+            for (int j = 0; j < QV; ++j) {
+                if (q0 + j < nq) ((TC *)P.c)[P.out_map.map(o2) + P.in_map.map(i2)] = narrow<TC>(acc[j]);
+                if (++i2 == (uint32_t)P.I) {
+                    i2 = 0;
+                    ++o2;
+                }
+            }
+            continue;
+        }
+        if (q0 + QV <= nq && ((q0 * (int64_t)sizeof(TC)) % (QV * (int64_t)sizeof(TC))) == 0 && QV * sizeof(TC) >= 8) {
+            if constexpr (QV * sizeof(TC) == 16) {
+                if constexpr (sizeof(TC) == 4) {
+                    *(float4 *)(out + q0) = make_float4(narrow<TC>(acc[0]), narrow<TC>(acc[1]), narrow<TC>(acc[2]), narrow<TC>(acc[3]));
+                } else {
+                    TC v2[2] = {narrow<TC>(acc[0]), narrow<TC>(acc[1])};
+                    *(uint4 *)(out + q0) = *(const uint4 *)v2;
+                }
+                continue;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < QV; ++j)
+            if (q0 + j < nq) out[q0 + j] = narrow<TC>(acc[j]);
+    }
+    pdl_release();
+}
+
 // ------------------------------------------------------------- regime S
 constexpr int kStages = 3;
 constexpr int kMaxOpt = 4;
@@ -1229,6 +1415,28 @@ static cudaError_t launch_rows_tma(const TtvLaunch &L, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kern, L.P, L.tmap);
 }
 
+template <class TA, class TC>
+static cudaError_t launch_short(const TtvLaunch &L, void *out, cudaStream_t st) {
+    if (L.vec == 4) {
+        if constexpr (sizeof(TC) == 4) {
+            ttv_short_kernel<TA, TC, 4><<<L.grid, L.block, 0, st>>>(L.P, (TC *)out);
+            return cudaGetLastError();
+        }
+    }
+    ttv_short_kernel<TA, TC, 2><<<L.grid, L.block, 0, st>>>(L.P, (TC *)out);
+    return cudaGetLastError();
+}
+
+// Regime 5: the short-fold stream, into C in canonical order (ident) or
+// through the digit maps (C's fastest canonical digit contiguous).
+static int ttv_short_run(const TtvLaunch &L, int32_t a_dtype, int32_t c_dtype, void *c_ptr, cudaStream_t st) {
+    cudaError_t e;
+    if (a_dtype == TL_F32 && c_dtype == TL_F32) e = launch_short<float, float>(L, c_ptr, st);
+    else if (a_dtype == TL_F32 && c_dtype == TL_F64) e = launch_short<float, double>(L, c_ptr, st);
+    else e = launch_short<double, double>(L, c_ptr, st);
+    return cuda_status(e, "ttv short-fold launch");
+}
+
 // Resident CTAs per SM of a kernel configuration (cached: no per-launch query)
 static cudaError_t occupancy(const void *kern, int threads, size_t smem, int &per_sm) {
     struct Entry {
@@ -1316,6 +1524,19 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         }
         return launch_kernel(kern, L, st);
     };
+    if (L.regime == 6) {
+        constexpr int VF = 16 / sizeof(TA);  // full 16-byte fibre pieces
+        if (L.P.I == 1) {
+            // 16-byte chunks along the rows when every row starts 16-byte aligned
+            if (L.vec > 1) return L.G == 16 ? go(ttv_deep_kernel<TA, TC, 2, true, 16>) : go(ttv_deep_kernel<TA, TC, 2, true, 8>);
+            return L.G == 16 ? go(ttv_deep_kernel<TA, TC, 1, true, 16>) : go(ttv_deep_kernel<TA, TC, 1, true, 8>);
+        }
+        if (L.vec == VF) return L.G == 16 ? go(ttv_deep_kernel<TA, TC, VF, false, 16>) : go(ttv_deep_kernel<TA, TC, VF, false, 8>);
+        if constexpr (VF == 4) {
+            if (L.vec == 2) return L.G == 16 ? go(ttv_deep_kernel<TA, TC, 2, false, 16>) : go(ttv_deep_kernel<TA, TC, 2, false, 8>);
+        }
+        return L.G == 16 ? go(ttv_deep_kernel<TA, TC, 1, false, 16>) : go(ttv_deep_kernel<TA, TC, 1, false, 8>);
+    }
     if (L.regime == 0) {
         constexpr int U = 8;
         const bool keep = L.P.l2_stream != 0;
@@ -1443,7 +1664,36 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
     return true;
 }
 
-static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch &L, Canon &cn) {
+// Long folds over too few fibres for the strided kernel's in-register loads
+// to fill HBM: the per-thread cp.async ring kernel (regime 6).  Fibres:
+// O*I/VEC (columns) or O rows when the contracted stride is 1.
+static void plan_deep(TtvLaunch &L, int64_t s, int nsm) {
+    static const int64_t min_k = [] {
+        const char *e = getenv("TL_TTV_DEEP_MIN_K");  // 0 disables the kernel
+        return (int64_t)(e ? atoll(e) : 256);
+    }();
+    TtvParams &P = L.P;
+    if (min_k <= 0 || P.K < min_k) return;
+    const bool rows = P.I == 1;
+    // rows: vec 2 marks 16-byte chunks (aligned rows), 1 element pieces otherwise
+    const int vec = rows ? ((((uintptr_t)P.a) % 16 == 0 && (P.K * s) % 16 == 0) ? 2 : 1) : L.vec;
+    const int64_t fibres = rows ? P.O : P.O * (P.I / vec);
+    // below ~128 fibres per SM the strided kernel's 8 loads in flight per
+    // thread cannot cover HBM latency (HOPM's 400^3 passes have 540 per SM
+    // and stay on it)
+    if (fibres >= (int64_t)nsm * 128) return;
+    const int ng = fibres >= (int64_t)nsm * 32 ? 8 : 16;  // deeper rings for fewer fibres
+    L.regime = 6;
+    L.vec = vec;
+    L.G = ng;
+    L.block = dim3(fibres >= (int64_t)nsm * 64 ? 64 : 32);
+    L.grid = dim3((unsigned)((fibres + L.block.x - 1) / L.block.x));
+    L.smem = (size_t)L.block.x * (ng * kDeepGroup * (16 + 16) + 16);  // A pieces + b values (<= 16 B each) + pad
+    (void)s;
+}
+
+static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch &L, Canon &cn, bool allow_short = true,
+                         bool allow_deep = true) {
     if (!canon_contraction(a, m0, 0, cn)) {
         set_error("ttv: operand A is not a dense permutation layout (materialise views first)");
         return TL_EUNSUPPORTED;
@@ -1469,6 +1719,33 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
     if (P.O * P.I == 0) return TL_OK;
     const uintptr_t base = (uintptr_t)P.a;
     bool ok;
+    // short folds of large tensors: an elementwise stream (+ a transpose when
+    // the output is permuted)
+    static const int64_t short_min = [] {
+        const char *e = getenv("TL_TTV_SHORT_MB");  // smallest operand (MB) taking the short-fold path; 0 = off
+        return (int64_t)(e ? atoll(e) : 64) << 20;
+    }();
+    // writes go straight to C when C is in canonical order (ident) or its
+    // fastest canonical digit is C-contiguous for at least 32 elements
+    // (whole 128-256-byte runs); other permuted outputs keep the tiled
+    // kernels below (a temporary + transpose measured slower there)
+    const DigitList &fast = cn.inner.empty() ? cn.outer : cn.inner;
+    const bool short_direct = cn.ident || (!fast.empty() && fast[0].second == 1 && fast[0].first >= 32);
+    // contracted stride 1 (rows of K): only the shortest rows -- from K ~ 8
+    // the staged kernel's tiles beat the per-thread L1 loads (K = 11: 0.94 vs 0.57)
+    const int64_t short_k = P.I == 1 ? 6 : kShortK;
+    if (allow_short && short_min > 0 && P.K <= short_k && P.O * P.K * P.I * (int64_t)s >= short_min && P.O * P.I < 0xffffffffll &&
+        a.dtype != TL_I64 && short_direct) {
+        L.regime = 5;
+        L.block = dim3(256);
+        const int qv = (s == 4) ? 4 : 2;
+        const int64_t threads = (P.O * P.I + qv - 1) / qv;
+        L.grid = dim3((unsigned)std::min<int64_t>((threads + 255) / 256, (int64_t)di.num_sms * 8));
+        L.vec = qv;
+        P.I_div.init((uint32_t)P.I);
+        L.smem = 0;
+        return TL_OK;
+    }
     const size_t small_bbytes = ((size_t)P.K * 8 + 15) & ~(size_t)15;
     // few outputs (<= 16384) of a small operand (<= 32 MB): latency-bound,
     // the whole-block kernels win (measured: config 1 5.6 -> 3.8 us)
@@ -1497,6 +1774,7 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
         ok = true;
     } else if (P.I >= 32) {
         ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
+        if (ok && allow_deep) plan_deep(L, (int64_t)s, di.num_sms);
     } else {
         ok = plan_staged(L, (int64_t)s, base, di.num_sms);
         if (ok && !P.ident && cn.outer.size() >= 3 && P.O * P.I < 0x7fffffffll) {
@@ -1515,7 +1793,10 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
                 L.grid = dim3((unsigned)std::min<int64_t>(P.ntiles, (int64_t)di.num_sms * per_sm));
             }
         }
-        if (!ok) ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
+        if (!ok) {
+            ok = plan_strided(L, (int64_t)s, base, di.num_sms, a.dtype);
+            if (ok && allow_deep) plan_deep(L, (int64_t)s, di.num_sms);
+        }
     }
     if (!ok) {
         set_error("ttv: no launch plan");
@@ -1530,6 +1811,8 @@ static const char *ttv_regime_name(const TtvLaunch &L) {
         case 1: return L.rows_tma ? "rows-tma" : (L.bulk ? "staged-bulk" : "staged");
         case 2: return "small-cols";
         case 4: return "strided-box";
+        case 5: return "short-fold";
+        case 6: return "deep-ring";
         default: return "small-rows";
     }
 }
@@ -1673,7 +1956,10 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         }
         return ttv_generic64_enqueue(a, a_ptr, cn, b_ptr, b_dtype, b_stride, c_dtype, c_ptr, stop, st);
     }
-    int rc = ttv_make_plan(a, a_ptr, m0, L, cn);
+    // the short-fold path (a stream + transpose) is for plain ttv calls, not
+    // the HOPM chains (stop flag, fused normalisation)
+    // the deep-ring kernel stages b in A's type
+    int rc = ttv_make_plan(a, a_ptr, m0, L, cn, stop == nullptr && (fn == nullptr || !fn->enabled), b_dtype == a.dtype);
     if (rc != TL_OK) return rc;
     TtvParams &P = L.P;
     if (P.O * P.I == 0) return TL_OK;
@@ -1726,6 +2012,7 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
             P.keep_tile = ntiles - std::min<int64_t>(ntiles, in_keep / (kRowsTmaR * P.K * s));
         }
     }
+    if (L.regime == 5) return ttv_short_run(L, a.dtype, c_dtype, c_ptr, st);
     cudaError_t e;
     if (a.dtype == TL_F32 && c_dtype == TL_F32) e = launch_typed<float, float>(L, st);
     else if (a.dtype == TL_F32 && c_dtype == TL_F64) e = launch_typed<float, double>(L, st);

@@ -1,11 +1,18 @@
-"""ttv over tensors at least twice the L2 size: these take the L2 streaming
+"""Large-tensor ttv paths, each checked bit for bit on integer-valued data
+(every fold exact in any order) against a float64 tensordot:
+
+* tensors at least twice the L2 size: these take the L2 streaming
 policy (loads evict-first except the part a pass reads last, which keeps the
 normal policy for the next pass over the same tensor; ttv.cu TtvParams::keep_*)
 -- in every instantiation it touches: the strided kernel for float32 (VEC 4 /
 2 / 1), float64 (VEC 2 / 1) and int64 (VEC 2 / 1) on one-wave and multi-wave
-grids, and the 2-D TMA rows kernel.  The policy must not change a result:
-integer-valued data makes every fold exact in any order, so each output is
-compared bit for bit with a float64 tensordot of the same data."""
+grids, and the 2-D TMA rows kernel -- the policy must not change a result;
+* short folds (K <= 16, >= 64 MB operands): the elementwise short-fold stream,
+  into C in canonical order or through the digit maps when C's fastest
+  canonical digit is contiguous;
+* long folds over few fibres: the per-thread cp.async ring kernel, columns
+  (VEC 4 / 1) and rows (16-byte chunks, and element pieces when rows are not
+  16-byte aligned)."""
 
 import pytest
 import torch
@@ -66,3 +73,43 @@ def test_ttv_large_tensor_l2_policy_exact(gpu, shape, dtype, modes):
         want = torch.tensordot(At, v.to(torch.float64), dims=([mode - 1], [0]))
         got = C.buffer.view(tuple(reversed(want.shape))).permute(*reversed(range(want.dim()))).to(torch.float64)
         assert torch.equal(got, want), f"{shape} {dtype} mode {mode}"
+
+
+CASES2 = [
+    # (shape, layout, dtype, mode, expected regime)
+    ((1848, 2, 21263), (2, 1, 3), torch.float64, 2, "short-fold"),  # K = 2, I = 1, ident
+    ((237, 10, 2, 11277), (3, 1, 4, 2), torch.float64, 3, "short-fold"),  # K = 2, permuted, fast digit C-contiguous
+    ((907, 24, 3, 1001), (1, 2, 3, 4), torch.float32, 3, "short-fold"),  # K = 3, I > 1
+    ((90, 4305, 336), (3, 2, 1), torch.float32, 2, "deep-ring"),  # few column fibres, long fold
+    ((45, 4305, 333), (3, 2, 1), torch.float32, 2, "deep-ring"),  # VEC 1 columns
+    ((201, 333367 // 4), (2, 1), torch.float64, 2, "deep-ring"),  # rows, odd K: element pieces
+    ((200, 83336), (2, 1), torch.float64, 2, "deep-ring"),  # rows, 16-byte chunks
+]
+
+
+@pytest.mark.parametrize("shape,layout,dtype,mode,regime", CASES2, ids=lambda v: str(v))
+def test_ttv_short_and_deep_paths_exact(gpu, shape, layout, dtype, mode, regime):
+    import ctypes
+    import json
+
+    m = tl()
+    n = 1
+    for e in shape:
+        n *= e
+    buf = small_ints(n, dtype, seed=n % 1000)
+    A = wrap(buf, shape, layout)
+    info = ctypes.create_string_buffer(512)
+    assert m._abi.lib().tl_plan_describe(0, A.desc(), None, mode, info, 512) == 0
+    assert json.loads(info.value.decode())["regime"] == regime
+    # torch view of the buffer: storage order = layout (dimension layout[0] fastest)
+    p = len(shape)
+    At = buf.view(tuple(shape[d - 1] for d in reversed(layout)))
+    perm = [0] * p
+    for pos, d in enumerate(reversed(layout)):
+        perm[d - 1] = pos
+    At = At.permute(*perm).to(torch.float64)
+    v = small_ints(shape[mode - 1], dtype, seed=7)
+    C = m.ttv(A, wrap(v, (shape[mode - 1],)), mode)
+    want = torch.tensordot(At, v.to(torch.float64), dims=([mode - 1], [0]))
+    got = C.buffer.view(tuple(reversed(want.shape))).permute(*reversed(range(want.dim()))).to(torch.float64)
+    assert torch.equal(got, want)

@@ -293,7 +293,12 @@ struct TtvBoxParams {
     int32_t b_dtype;
     int32_t b_smem;
     int64_t K, I;           // contracted extent and its A stride
-    int64_t e0, cs0;        // d0: extent and C stride (A stride 1)
+    int64_t e0, cs0;        // A-direction: extent (of the A-chain) and, for a one-digit chain, its C stride
+    // A-chain of more than one digit (a prefix of the inner digits, contiguous
+    // in A): position -> C offset through this digit map (na > 1)
+    int32_t na;
+    FastDiv a_div[kBoxMaxChain];
+    int64_t a_cs[kBoxMaxChain];
     int64_t nA, nJ, nrest;  // box counts along d0, along the chain, other digits
     int64_t chain_ext;
     int32_t nchain;
@@ -318,7 +323,8 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
     const size_t bbytes = P.b_smem ? (((size_t)P.K * sizeof(Acc) + 15) & ~(size_t)15) : 0;
     int64_t *tabA = (int64_t *)(smem_raw + bbytes);
     int64_t *tabC = tabA + BC;
-    Acc *otile = (Acc *)(tabC + BC);  // [BC][PITCH]
+    TC *otile = (TC *)(tabC + BC);  // [BC][PITCH], already in C's type (the narrowing is the store's)
+    int64_t *tabAC = (int64_t *)(smem_raw + bbytes + 2 * BC * 8 + ((BC * PITCH * sizeof(TC) + 7) & ~(size_t)7));  // [BA]
     if (P.b_smem) {
         for (int64_t k = threadIdx.x; k < P.K; k += blockDim.x) bs[k] = load_elem_as<Acc>(P.b, P.b_dtype, k * P.b_stride);
     }
@@ -332,7 +338,7 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
         const int64_t t2 = tile / P.nA;
         const int64_t jb = t2 % P.nJ;
         uint32_t rest = (uint32_t)(t2 / P.nJ);
-        int64_t baseA = ab * BA, baseC = ab * BA * P.cs0;
+        int64_t baseA = ab * BA, baseC = P.na > 1 ? 0 : ab * BA * P.cs0;
         for (int d = 0; d < P.nrest_d; ++d) {
             uint32_t q, r;
             if (d == P.nrest_d - 1) {
@@ -346,6 +352,23 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
             rest = q;
         }
         __syncthreads();  // the previous tile's write-out is done with tabC / otile
+        if (P.na > 1 && threadIdx.x < BA) {
+            // C offset of A-chain position ab*BA + threadIdx.x
+            uint32_t x = (uint32_t)(ab * BA + threadIdx.x);
+            int64_t oc = 0;
+            for (int d = 0; d < P.na; ++d) {
+                uint32_t q, r;
+                if (d == P.na - 1) {
+                    r = x;
+                    q = 0;
+                } else {
+                    P.a_div[d].divmod(x, q, r);
+                }
+                oc += (int64_t)r * P.a_cs[d];
+                x = q;
+            }
+            tabAC[threadIdx.x] = oc;
+        }
         if (threadIdx.x < BC) {
             const int64_t jg = jb * BC + threadIdx.x;
             int64_t oa = -1, oc = 0;
@@ -404,14 +427,14 @@ __global__ void __launch_bounds__(256) ttv_box_kernel(const __grid_constant__ Tt
                 }
             }
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) otile[j * PITCH + a + v] = acc[v];
+            for (int v = 0; v < VEC; ++v) otile[j * PITCH + a + v] = narrow<TC>(acc[v]);
         }
         __syncthreads();
         // write out along the C-contiguous chain
         for (int idx = threadIdx.x; idx < BA * BC; idx += blockDim.x) {
             const int j = idx % BC, aa = idx / BC;
             if (tabA[j] >= 0 && ab * BA + aa < P.e0)
-                C[baseC + aa * P.cs0 + tabC[j]] = narrow<TC>(otile[j * PITCH + aa]);
+                C[baseC + (P.na > 1 ? tabAC[aa] : aa * P.cs0) + tabC[j]] = otile[j * PITCH + aa];
         }
     }
     pdl_release();
@@ -1564,7 +1587,7 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
 // Regime-B plan with a permuted output: the boxed kernel when A's fastest
 // free digit d0 is not C's fastest and a C-contiguous chain of at least 16
 // positions exists among the other free digits.
-static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
+static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, int64_t cs_elem) {
     static const bool off = getenv("TL_TTV_NO_BOX") != nullptr;
     if (off || cn.ident || cn.inner.empty()) return false;
     // Measured on B200: the box's 8 warps stream 8 separate A regions, which
@@ -1588,8 +1611,10 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
         }
     }
     const Dg d0 = free[0];
-    if (d0.ext < 16) return false;
-    // the C-fastest other digit, then digits continuing its C run
+    const size_t ninner = cn.inner.size();
+    // the C-fastest digit other than d0 (A's fastest), then digits continuing
+    // its C run; the A-direction is then the prefix of the inner digits (all
+    // contiguous in A) before the first one the C-chain uses
     int cstar = -1;
     for (size_t q = 1; q < free.size(); ++q)
         if (cstar < 0 || free[q].cs < free[cstar].cs) cstar = (int)q;
@@ -1608,12 +1633,26 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
         cext *= free[nxt].ext;
     }
     if (cext < 16 || cext > 0xffffffffll) return false;
+    // A-chain: inner digits [0, na) -- d0 alone when it is long enough (the
+    // tuned one-digit box), else as many inner digits as precede the C-chain
+    size_t na = d0.ext >= 16 ? 1 : ninner;
+    for (int q : chain)
+        if ((size_t)q < na) na = (size_t)q;
+    if (na == 0 || na > (size_t)kBoxMaxChain) return false;
+    int64_t ea = 1;
+    for (size_t q = 0; q < na; ++q) ea *= free[q].ext;
+    if (ea < 16 || ea > 0xffffffffll) return false;
     TtvBoxParams &B = L.box;
     B = TtvBoxParams{};
     B.K = cn.K;
     B.I = cn.I;
-    B.e0 = d0.ext;
+    B.e0 = ea;
     B.cs0 = d0.cs;
+    B.na = (int32_t)na;
+    for (size_t q = 0; q < na; ++q) {
+        B.a_div[q].init((uint32_t)free[q].ext);
+        B.a_cs[q] = free[q].cs;
+    }
     B.chain_ext = cext;
     B.nchain = (int32_t)chain.size();
     for (size_t q = 0; q < chain.size(); ++q) {
@@ -1623,7 +1662,7 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
     }
     int64_t nrest = 1;
     B.nrest_d = 0;
-    for (size_t q = 1; q < free.size(); ++q) {
+    for (size_t q = na; q < free.size(); ++q) {
         if (std::find(chain.begin(), chain.end(), (int)q) != chain.end()) continue;
         if (free[q].ext > 0xffffffffll) return false;
         B.rs_div[B.nrest_d].init((uint32_t)free[q].ext);
@@ -1638,17 +1677,17 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
         B.nrest_d = 1;
     }
     int vec = 1;
-    if (s == 4 && d0.ext % 4 == 0 && base_addr % 16 == 0 && (cn.I % 4) == 0) vec = 4;
-    else if (d0.ext % 2 == 0 && base_addr % (2 * s) == 0 && (cn.I % 2) == 0 && s <= 8) vec = 2;
+    if (s == 4 && ea % 4 == 0 && base_addr % 16 == 0 && (cn.I % 4) == 0) vec = 4;
+    else if (ea % 2 == 0 && base_addr % (2 * s) == 0 && (cn.I % 2) == 0 && s <= 8) vec = 2;
     static const int box_h_env = [] {
         const char *e = getenv("TL_TTV_BOX_H");
         return e ? atoi(e) : 2;
     }();
     // two warps per chain row (1 KB runs along d0) for float64 pairs when d0 is long enough
-    const int h = (box_h_env == 2 && vec == 2 && s == 8 && d0.ext >= 128) ? 2 : 1;
+    const int h = (box_h_env == 2 && vec == 2 && s == 8 && ea >= 128) ? 2 : 1;
     L.box_h = h;
     const int64_t BA = 32 * vec * h, BC = 64 / h;
-    B.nA = (d0.ext + BA - 1) / BA;
+    B.nA = (ea + BA - 1) / BA;
     B.nJ = (cext + BC - 1) / BC;
     B.nrest = nrest;
     const int64_t ntiles = B.nA * B.nJ * B.nrest;
@@ -1658,8 +1697,8 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
     L.vec = vec;
     L.block = dim3(256);
     const size_t bbytes = B.b_smem ? (((size_t)cn.K * 8 + 15) & ~(size_t)15) : 0;
-    L.smem = bbytes + 2 * BC * 8 + (size_t)BC * (BA + 1) * 8;
-    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / ((int64_t)L.smem + 2048)));
+    L.smem = bbytes + 2 * BC * 8 + (((size_t)BC * (BA + 1) * cs_elem + 7) & ~(size_t)7) + (size_t)BA * 8;
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (228 * 1024) / ((int64_t)L.smem + 2048)));
     L.grid = dim3((unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * per_sm * 2));
     return true;
 }
@@ -1830,7 +1869,7 @@ int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len) {
     }
     int rc = ttv_make_plan(a, (const void *)0x100000, m0, L, cn);
     if (rc != TL_OK) return rc;
-    if (L.regime == 0) plan_box(cn, L, (int64_t)dtype_size(a.dtype), 0x100000, device_info().num_sms);
+    if (L.regime == 0) plan_box(cn, L, (int64_t)dtype_size(a.dtype), 0x100000, device_info().num_sms, (int64_t)dtype_size(a.dtype));
     if (L.regime == 1) plan_rows_tma(L, cn, a.dtype, device_info().num_sms);  // needs the driver's encoder
     snprintf(buf, len, "{\"O\": %lld, \"K\": %lld, \"I\": %lld, \"ident\": %d, \"inner_digits\": %d, "
              "\"outer_digits\": %d, \"regime\": \"%s\", \"vec\": %d, \"grid\": %u, \"block\": %u, \"smem\": %zu}",
@@ -1986,7 +2025,7 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         // contracted stride 1: rows through the 2-D TMA tensor map
     } else if (L.regime == 0) {
         // permuted output on the strided regime: the boxed kernel
-        if (plan_box(cn, L, (int64_t)dtype_size(a.dtype), (uintptr_t)P.a, device_info().num_sms)) {
+        if (plan_box(cn, L, (int64_t)dtype_size(a.dtype), (uintptr_t)P.a, device_info().num_sms, (int64_t)dtype_size(c_dtype))) {
             TtvBoxParams &B = L.box;
             B.a = P.a;
             B.b = b_ptr;

@@ -745,6 +745,105 @@ __global__ void __launch_bounds__(64) ttv_deep_kernel(const __grid_constant__ Tt
     pdl_release();
 }
 
+// ------------------------------------------------------------- short folds, permuted outputs
+// K <= kShortK with a permuted output whose fastest canonical digit is not
+// C-contiguous: the output (N/K elements) would be written scattered.  A CTA
+// folds a TX x TY tile of outputs -- TY positions along a chain of free
+// digits contiguous in A (the inner digits, or for a contracted stride of 1
+// the rows), TX along a chain contiguous in C -- parks it in shared memory
+// and writes it out along C (a transpose fused with the fold).  Chains are
+// flat index spaces split into blocks; per-tile tables hold the A and C
+// offsets of their positions.  Each output's k order is unchanged (bit-exact).
+struct TtvTileParams {
+    const void *a;
+    const void *b;
+    void *c;
+    const int32_t *stop;
+    int64_t b_stride;
+    int32_t b_dtype;
+    int64_t K, I;
+    int64_t ex, ey;              // chain extents
+    int64_t nxb, nyb, nrest;     // blocks along each chain, other positions
+    DigitMap xa, xc, ya, yc, ra, rc;  // A / C offsets of chain and rest indices
+};
+constexpr int kTileX = 64, kTileY = 128;  // largest tile shape (the planner's chain targets)
+constexpr int kShortK = 16;  // folds this short take the short-fold / tile-fold streams
+
+template <class TA, class TC, int TX, int TY>
+__global__ void __launch_bounds__(256) ttv_tile_kernel(const __grid_constant__ TtvTileParams P) {
+    using Acc = typename AccOf<TA>::type;
+    constexpr int JX = TX * TY / 256;
+    __shared__ int64_t tXA[TX], tXC[TX], tYA[TY], tYC[TY];
+    __shared__ Acc bs[kShortK];
+    __shared__ TC tile[TX][TY + 1];
+    pdl_wait();
+    if (stop_requested(P.stop)) return;
+    const int K = (int)P.K;
+    if (threadIdx.x < K) bs[threadIdx.x] = load_elem_as<Acc>(P.b, P.b_dtype, threadIdx.x * P.b_stride);
+    const TA *A = (const TA *)P.a;
+    TC *C = (TC *)P.c;
+    const int64_t ntiles = P.nxb * P.nyb * P.nrest;
+    const int tid = threadIdx.x;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t yb = t % P.nyb;
+        const int64_t t2 = t / P.nyb;
+        const int64_t xb = t2 % P.nxb;
+        const uint32_t rest = (uint32_t)(t2 / P.nxb);
+        __syncthreads();  // the previous tile is written out; b is staged
+        if (tid < TY) {
+            const int64_t y = yb * TY + tid;
+            tYA[tid] = y < P.ey ? P.ya.map((uint32_t)y) : -1;
+            tYC[tid] = y < P.ey ? P.yc.map((uint32_t)y) : 0;
+        } else if (tid < TY + TX) {
+            const int64_t x = xb * TX + (tid - TY);
+            tXA[tid - TY] = x < P.ex ? P.xa.map((uint32_t)x) : -1;
+            tXC[tid - TY] = x < P.ex ? P.xc.map((uint32_t)x) : 0;
+        }
+        const int64_t rA = P.ra.map(rest), rC = P.rc.map(rest);
+        __syncthreads();
+        // fold: lanes along y (A-contiguous), JX outputs per thread, all of
+        // a k's loads issued together
+        {
+            const int y = tid % TY;
+            const int x0 = tid / TY;
+            constexpr int XS = 256 / TY;
+            Acc acc[JX];
+            const TA *pa[JX];
+            bool ok[JX];
+#pragma unroll
+            for (int j = 0; j < JX; ++j) {
+                const int x = x0 + XS * j;
+                ok[j] = tYA[y] >= 0 && tXA[x] >= 0;
+                pa[j] = A + rA + (ok[j] ? tXA[x] + tYA[y] : 0);
+                acc[j] = Acc(0);
+            }
+            for (int k = 0; k < K; ++k) {
+                const Acc bk = bs[k];
+                TA v[JX];
+#pragma unroll
+                for (int j = 0; j < JX; ++j) v[j] = ok[j] ? __ldg(pa[j] + (int64_t)k * P.I) : TA(0);
+#pragma unroll
+                for (int j = 0; j < JX; ++j) acc[j] = fold_step(acc[j], (Acc)v[j], bk);
+            }
+#pragma unroll
+            for (int j = 0; j < JX; ++j) tile[x0 + XS * j][y] = narrow<TC>(acc[j]);
+        }
+        __syncthreads();
+        // write out: lanes along x (C-contiguous)
+        {
+            const int x = tid % TX;
+            const int y0 = tid / TX;
+            constexpr int YS = 256 / TX;
+#pragma unroll
+            for (int j = 0; j < TY / YS; ++j) {
+                const int y = y0 + YS * j;
+                if (tXA[x] >= 0 && tYA[y] >= 0) C[rC + tXC[x] + tYC[y]] = tile[x][y];
+            }
+        }
+    }
+    pdl_release();
+}
+
 // ------------------------------------------------------------- short folds
 // K <= kShortK over a large tensor: the output is a sizeable fraction of the
 // input (N/K), so the contraction is an elementwise stream.  Each thread
@@ -754,8 +853,6 @@ __global__ void __launch_bounds__(64) ttv_deep_kernel(const __grid_constant__ Tt
 // permuted outputs stay on the tiled kernels: a temporary + transpose
 // measured slower there).  The loads go through L1: neighbouring threads and
 // k's share sectors.
-constexpr int kShortK = 16;
-
 template <class TA, class TC, int QV>
 __global__ void __launch_bounds__(256) ttv_short_kernel(const __grid_constant__ TtvParams P, TC *out) {
     // out == nullptr: permuted C written through the digit maps (its fastest
@@ -1178,6 +1275,7 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
 struct TtvLaunch {
     TtvParams P;
     TtvBoxParams box;  // regime 4
+    TtvTileParams tile;  // regime 7
     int regime;  // 0 = strided (B), 1 = staged (S), 2/3 = small, 4 = boxed strided
     int vec;
     int G;
@@ -1484,6 +1582,24 @@ static cudaError_t occupancy(const void *kern, int threads, size_t smem, int &pe
 template <class TA, class TC>
 static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
     if (L.regime == 4) return launch_box<TA, TC>(L, st);
+    if (L.regime == 7) {
+        if constexpr (std::is_same<TA, int64_t>::value) {
+            return cudaErrorInvalidValue;
+        } else {
+            switch (L.G) {
+                case 1: ttv_tile_kernel<TA, TC, 64, 64><<<L.grid, L.block, 0, st>>>(L.tile); break;
+                case 2: ttv_tile_kernel<TA, TC, 32, 128><<<L.grid, L.block, 0, st>>>(L.tile); break;
+                case 3:
+                    if constexpr (sizeof(TC) == 4) {
+                        ttv_tile_kernel<TA, TC, 64, 128><<<L.grid, L.block, 0, st>>>(L.tile);
+                        break;
+                    }
+                    return cudaErrorInvalidValue;  // 64 KB of float64 tile: planned only for float32
+                default: ttv_tile_kernel<TA, TC, 32, 64><<<L.grid, L.block, 0, st>>>(L.tile); break;
+            }
+            return cudaGetLastError();
+        }
+    }
     if (L.rows_tma) {
         if constexpr (std::is_same<TA, float>::value || std::is_same<TA, double>::value) return launch_rows_tma<TA, TC>(L, st);
         return cudaErrorInvalidValue;
@@ -1703,6 +1819,104 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
     return true;
 }
 
+// Regime 7 plan: the fused transpose-fold for short folds with a permuted
+// output.  Digits: (extent, A stride, C stride) in A order.
+static bool plan_tile(const Canon &cn, TtvLaunch &L, int nsm, bool s8) {
+    static const bool off = getenv("TL_TTV_NO_TILE") != nullptr;
+    if (off) return false;
+    struct Dg {
+        int64_t ext, as, cs;
+    };
+    std::vector<Dg> F;
+    int64_t run = 1;
+    for (auto &d : cn.inner) {
+        F.push_back({d.first, run, d.second});
+        run *= d.first;
+    }
+    run = cn.K * cn.I;
+    for (auto &d : cn.outer) {
+        F.push_back({d.first, run, d.second});
+        run *= d.first;
+    }
+    const size_t nf = F.size();
+    if (nf < 2) return false;
+    std::vector<int> used(nf, 0);
+    static const int shape = getenv("TL_TTV_TILE_SHAPE") ? atoi(getenv("TL_TTV_TILE_SHAPE")) : 0;
+    const int sh = (shape == 3 && s8) ? 1 : (shape & 3);  // 64 x 128 tiles only for 4-byte outputs
+    const int tx = (sh & 1) ? 64 : 32, ty = (sh & 2) ? 128 : 64;
+    // the C-fastest digit heads the X chain; Y: A-fastest digits before it
+    // (inner, then outer when the inner block is short)
+    int c0 = 0;
+    for (size_t q = 1; q < nf; ++q)
+        if (F[q].cs < F[c0].cs) c0 = (int)q;
+    std::vector<int> ych;
+    int64_t ey = 1;
+    for (size_t q = 0; q < nf && ey < ty && (int)q != c0; ++q) {
+        if (q == cn.inner.size() && ey >= 16) break;  // do not cross the k gap once Y is usable
+        ych.push_back((int)q);
+        used[q] = 1;
+        ey *= F[q].ext;
+    }
+    // X: C-fastest remaining digit, then digits continuing its C run
+    std::vector<int> xch;
+    int64_t ex = 1;
+    {
+        int cstar = -1;
+        for (size_t q = 0; q < nf; ++q)
+            if (!used[q] && (cstar < 0 || F[q].cs < F[cstar].cs)) cstar = (int)q;
+        if (cstar < 0) return false;
+        xch.push_back(cstar);
+        used[cstar] = 1;
+        ex = F[cstar].ext;
+        while (ex < tx) {
+            const Dg &last = F[xch.back()];
+            int nxt = -1;
+            for (size_t q = 0; q < nf; ++q)
+                if (!used[q] && F[q].cs == last.cs * last.ext) nxt = (int)q;
+            if (nxt < 0) break;
+            xch.push_back(nxt);
+            used[nxt] = 1;
+            ex *= F[nxt].ext;
+        }
+    }
+    if (ex < 8 || ey < 16 || ex > 0xffffffffll || ey > 0xffffffffll) return false;
+    DigitList ya, yc, xa, xc, ra, rc;
+    for (int q : ych) {
+        ya.push_back({F[q].ext, F[q].as});
+        yc.push_back({F[q].ext, F[q].cs});
+    }
+    for (int q : xch) {
+        xa.push_back({F[q].ext, F[q].as});
+        xc.push_back({F[q].ext, F[q].cs});
+    }
+    int64_t nrest = 1;
+    for (size_t q = 0; q < nf; ++q)
+        if (!used[q]) {
+            ra.push_back({F[q].ext, F[q].as});
+            rc.push_back({F[q].ext, F[q].cs});
+            nrest *= F[q].ext;
+        }
+    TtvTileParams &T = L.tile;
+    T = TtvTileParams{};
+    if (!build_map(ya, T.ya) || !build_map(yc, T.yc) || !build_map(xa, T.xa) || !build_map(xc, T.xc) ||
+        !build_map(ra, T.ra) || !build_map(rc, T.rc) || nrest > 0xffffffffll)
+        return false;
+    T.K = cn.K;
+    T.I = cn.I;
+    T.ex = ex;
+    T.ey = ey;
+    L.G = sh;
+    T.nxb = (ex + tx - 1) / tx;
+    T.nyb = (ey + ty - 1) / ty;
+    T.nrest = nrest;
+    const int64_t ntiles = T.nxb * T.nyb * T.nrest;
+    L.regime = 7;
+    L.block = dim3(256);
+    L.grid = dim3((unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * 8));
+    L.smem = 0;
+    return true;
+}
+
 // Long folds over too few fibres for the strided kernel's in-register loads
 // to fill HBM: the per-thread cp.async ring kernel (regime 6).  Fibres:
 // O*I/VEC (columns) or O rows when the contracted stride is 1.
@@ -1785,6 +1999,10 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
         L.smem = 0;
         return TL_OK;
     }
+    // (K <= 4: from K ~ 9 the boxed / staged kernels do better, config 5)
+    if (allow_short && short_min > 0 && P.K <= 4 && !cn.ident && P.O * P.K * P.I * (int64_t)s >= short_min &&
+        a.dtype != TL_I64 && plan_tile(cn, L, di.num_sms, s == 8))
+        return TL_OK;
     const size_t small_bbytes = ((size_t)P.K * 8 + 15) & ~(size_t)15;
     // few outputs (<= 16384) of a small operand (<= 32 MB): latency-bound,
     // the whole-block kernels win (measured: config 1 5.6 -> 3.8 us)
@@ -1852,6 +2070,7 @@ static const char *ttv_regime_name(const TtvLaunch &L) {
         case 4: return "strided-box";
         case 5: return "short-fold";
         case 6: return "deep-ring";
+        case 7: return "tile-fold";
         default: return "small-rows";
     }
 }
@@ -2052,6 +2271,15 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
         }
     }
     if (L.regime == 5) return ttv_short_run(L, a.dtype, c_dtype, c_ptr, st);
+    if (L.regime == 7) {
+        TtvTileParams &T = L.tile;
+        T.a = P.a;
+        T.b = b_ptr;
+        T.c = c_ptr;
+        T.stop = stop;
+        T.b_stride = b_stride;
+        T.b_dtype = b_dtype;
+    }
     cudaError_t e;
     if (a.dtype == TL_F32 && c_dtype == TL_F32) e = launch_typed<float, float>(L, st);
     else if (a.dtype == TL_F32 && c_dtype == TL_F64) e = launch_typed<float, double>(L, st);

@@ -84,6 +84,12 @@ CASES2 = [
     ((45, 4305, 333), (3, 2, 1), torch.float32, 2, "deep-ring"),  # VEC 1 columns
     ((201, 333367 // 4), (2, 1), torch.float64, 2, "deep-ring"),  # rows, odd K: element pieces
     ((200, 83336), (2, 1), torch.float64, 2, "deep-ring"),  # rows, 16-byte chunks
+    # short folds with scattered permuted outputs: the fused transpose-fold
+    ((7, 3, 6, 3, 20, 36, 551), (3, 5, 1, 4, 7, 6, 2), torch.float32, 4, "tile-fold"),  # K = 3, short X chain
+    ((5, 4, 532, 801, 2, 8), (2, 6, 4, 3, 5, 1), torch.float32, 2, "tile-fold"),  # rows of K = 4
+    ((2, 5, 4305, 56, 6, 9), (5, 4, 3, 1, 2, 6), torch.float32, 1, "tile-fold"),  # K = 2, long inner block
+    ((6, 29, 7, 11, 2, 634, 10), (7, 5, 3, 6, 1, 2, 4), torch.float32, 5, "tile-fold"),  # K = 2, I = 10
+    ((15, 42, 2, 4, 22, 5, 147), (5, 1, 2, 3, 7, 6, 4), torch.float64, 3, "tile-fold"),  # float64, K = 2
 ]
 
 

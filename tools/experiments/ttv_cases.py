@@ -30,6 +30,7 @@ CASES = [
     ("h", torch.float32, (2, 5, 4305, 56, 6, 9), (5, 4, 3, 1, 2, 6), 3),
     ("i", torch.float64, (201, 333367), (2, 1), 2),
     ("j", torch.float32, (189286, 709), (2, 1), 1),
+    ("k", torch.float64, (15, 42, 2, 4, 22, 5, 147), (5, 1, 2, 3, 7, 6, 4), 3),
     ("cfg5s0", torch.float64, (3, 33, 5, 17, 9, 2, 640), (5, 3, 2, 1, 6, 4, 7), 5),
     ("cfg5s5", torch.float64, (3, 33, 5, 17, 9, 2, 640), (7, 4, 2, 1, 6, 3, 5), 5),
 ]

@@ -1271,6 +1271,82 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
     pdl_release();
 }
 
+// Long folds over few column fibres (contracted stride I >= a few 16-byte
+// vectors, 16-byte-aligned rows): one warp per CTA owns BI consecutive
+// outputs (o, i0..i0+BI-1); slabs of BK k-rows x BI columns stream through a
+// 4-stage 2-D TMA pipeline (one elected lane issues each box onto the
+// stage's mbarrier; columns past I are zero-filled by the tensor map), and
+// lane l folds column l in k order from shared memory (bit-exact).  b comes
+// in per slab as two coalesced loads and is broadcast with shuffles.  Many
+// one-warp CTAs per SM: per-thread instruction latency is hidden across them,
+// the data is in flight as whole boxes (no per-element copies).
+constexpr int kColsBI = 32, kColsStages = 4;
+__host__ __device__ constexpr int cols_bk(int elem) { return elem == 4 ? 64 : 32; }  // 32 KB of stages either way
+
+template <class TA, class TC>
+__global__ void __launch_bounds__(32) ttv_cols_tma_kernel(const __grid_constant__ TtvParams P,
+                                                          const __grid_constant__ CUtensorMap map) {
+    using Acc = typename AccOf<TA>::type;
+    constexpr int BI = kColsBI, BK = cols_bk((int)sizeof(TA)), NST = kColsStages;
+    __shared__ __align__(128) TA st[NST][BK][BI];
+    __shared__ __align__(8) uint64_t full_bar[NST];
+    pdl_wait();
+    if (stop_requested(P.stop)) return;
+    const int lane = threadIdx.x;
+    const int64_t K = P.K, I = P.I;
+    const int64_t nib = (I + BI - 1) / BI;
+    const int64_t o = blockIdx.x / nib;
+    const int64_t i0 = (blockIdx.x - o * nib) * BI;
+    const int nslab = (int)((K + BK - 1) / BK);
+    if (lane == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(&full_bar[s], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    auto issue = [&](int slab) {
+        if (lane == 0 && slab < nslab) {
+            const int s = slab % NST;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(BK * BI * sizeof(TA)));
+            tma_load_2d(&st[s][0][0], &map, (int32_t)i0, (int32_t)(o * K + (int64_t)slab * BK), &full_bar[s]);
+        }
+    };
+    for (int s = 0; s < NST; ++s) issue(s);
+    Acc acc = Acc(0);
+    uint32_t parity = 0;
+    for (int slab = 0; slab < nslab; ++slab) {
+        const int s = slab % NST;
+        const int64_t k0 = (int64_t)slab * BK;
+        // this slab's b: lane l holds b[k0 + l] and b[k0 + 32 + l]
+        const Acc b0 = k0 + lane < K ? load_elem_as<Acc>(P.b, P.b_dtype, (k0 + lane) * P.b_stride) : Acc(0);
+        const Acc b1 = (BK > 32 && k0 + 32 + lane < K) ? load_elem_as<Acc>(P.b, P.b_dtype, (k0 + 32 + lane) * P.b_stride) : Acc(0);
+        mbar_wait_parity(&full_bar[s], parity);
+        const int kn = (int)(K - k0 < BK ? K - k0 : BK);
+        if (kn == BK) {
+#pragma unroll 16
+            for (int kk = 0; kk < BK; ++kk) {
+                const Acc bk = __shfl_sync(0xffffffffu, kk < 32 ? b0 : b1, kk & 31);
+                acc = fold_step(acc, (Acc)st[s][kk][lane], bk);
+            }
+        } else {
+            for (int kk = 0; kk < kn; ++kk) {
+                const Acc bk = __shfl_sync(0xffffffffu, kk < 32 ? b0 : b1, kk & 31);
+                acc = fold_step(acc, (Acc)st[s][kk][lane], bk);
+            }
+        }
+        __syncwarp();  // every lane is done with stage s
+        issue(slab + NST);
+        if (s == NST - 1) parity ^= 1u;
+    }
+    const int64_t i = i0 + lane;
+    if (i < I) {
+        TC *c = (TC *)P.c;
+        const int64_t off = P.ident ? o * I + i : P.out_map.map((uint32_t)o) + P.in_map.map((uint32_t)i);
+        c[off] = narrow<TC>(acc);
+    }
+    pdl_release();
+}
+
 // ------------------------------------------------------------- planning
 struct TtvLaunch {
     TtvParams P;
@@ -1663,6 +1739,14 @@ static cudaError_t launch_typed(const TtvLaunch &L, cudaStream_t st) {
         }
         return launch_kernel(kern, L, st);
     };
+    if (L.regime == 8) {
+        if constexpr (std::is_same<TA, float>::value || std::is_same<TA, double>::value) {
+            // plain stream order even in a PDL chain (griddepcontrol is then a no-op)
+            ttv_cols_tma_kernel<TA, TC><<<L.grid, L.block, 0, st>>>(L.P, L.tmap);
+            return cudaGetLastError();
+        }
+        return cudaErrorInvalidValue;
+    }
     if (L.regime == 6) {
         constexpr int VF = 16 / sizeof(TA);  // full 16-byte fibre pieces
         if (L.P.I == 1) {
@@ -1917,6 +2001,33 @@ static bool plan_tile(const Canon &cn, TtvLaunch &L, int nsm, bool s8) {
     return true;
 }
 
+// Regime 8: few column fibres, long fold, 16-byte-aligned rows -> 2-D TMA
+// boxes of kColsBK k-rows x kColsBI columns over A viewed as (K*O) x I.
+static bool plan_cols_tma(TtvLaunch &L, int64_t s) {
+    static const bool off = getenv("TL_TTV_NO_COLS_TMA") != nullptr;
+    TtvParams &P = L.P;
+    if (off || (s != 4 && s != 8)) return false;
+    const uintptr_t base = (uintptr_t)P.a;
+    if (base % 16 != 0 || (P.I * s) % 16 != 0 || P.I * s < 16 || P.O * P.K > 0x7fffffffll || P.I > 0x7fffffffll) return false;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+    if (enc == nullptr) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)P.I, (cuuint64_t)(P.O * P.K)};
+    const cuuint64_t strides[1] = {(cuuint64_t)(P.I * s)};
+    const cuuint32_t box[2] = {(cuuint32_t)kColsBI, (cuuint32_t)cols_bk((int)s)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&L.tmap, s == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)P.a,
+                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    const int64_t nib = (P.I + kColsBI - 1) / kColsBI;
+    if (P.O * nib > 0x7fffffffll) return false;
+    L.regime = 8;
+    L.block = dim3(32);
+    L.grid = dim3((unsigned)(P.O * nib));
+    L.smem = 0;
+    return true;
+}
+
 // Long folds over too few fibres for the strided kernel's in-register loads
 // to fill HBM: the per-thread cp.async ring kernel (regime 6).  Fibres:
 // O*I/VEC (columns) or O rows when the contracted stride is 1.
@@ -1935,6 +2046,7 @@ static void plan_deep(TtvLaunch &L, int64_t s, int nsm) {
     // thread cannot cover HBM latency (HOPM's 400^3 passes have 540 per SM
     // and stay on it)
     if (fibres >= (int64_t)nsm * 128) return;
+    if (!rows && plan_cols_tma(L, s)) return;
     const int ng = fibres >= (int64_t)nsm * 32 ? 8 : 16;  // deeper rings for fewer fibres
     L.regime = 6;
     L.vec = vec;
@@ -2071,6 +2183,7 @@ static const char *ttv_regime_name(const TtvLaunch &L) {
         case 5: return "short-fold";
         case 6: return "deep-ring";
         case 7: return "tile-fold";
+        case 8: return "cols-tma";
         default: return "small-rows";
     }
 }

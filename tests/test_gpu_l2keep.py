@@ -10,9 +10,10 @@ grids, and the 2-D TMA rows kernel -- the policy must not change a result;
 * short folds (K <= 16, >= 64 MB operands): the elementwise short-fold stream,
   into C in canonical order or through the digit maps when C's fastest
   canonical digit is contiguous;
-* long folds over few fibres: the per-thread cp.async ring kernel, columns
-  (VEC 4 / 1) and rows (16-byte chunks, and element pieces when rows are not
-  16-byte aligned)."""
+* long folds over few fibres: one-warp CTAs streaming 2-D TMA boxes of k-rows x
+  32 columns when rows are 16-byte aligned, else the per-thread cp.async ring
+  kernel, columns (VEC 4 / 1) and rows (16-byte chunks, and element pieces
+  when rows are not 16-byte aligned)."""
 
 import pytest
 import torch
@@ -80,7 +81,9 @@ CASES2 = [
     ((1848, 2, 21263), (2, 1, 3), torch.float64, 2, "short-fold"),  # K = 2, I = 1, ident
     ((237, 10, 2, 11277), (3, 1, 4, 2), torch.float64, 3, "short-fold"),  # K = 2, permuted, fast digit C-contiguous
     ((907, 24, 3, 1001), (1, 2, 3, 4), torch.float32, 3, "short-fold"),  # K = 3, I > 1
-    ((90, 4305, 336), (3, 2, 1), torch.float32, 2, "deep-ring"),  # few column fibres, long fold
+    ((90, 4305, 336), (3, 2, 1), torch.float32, 2, "cols-tma"),  # few column fibres, long fold, aligned rows
+    ((128, 4096, 64), (1, 2, 3), torch.float64, 2, "cols-tma"),  # float64 boxes; last slab zero-padded by TMA past I
+    ((101, 3000, 97), (1, 2, 3), torch.float64, 2, "deep-ring"),  # I*8 not 16-byte aligned: the ring
     ((45, 4305, 333), (3, 2, 1), torch.float32, 2, "deep-ring"),  # VEC 1 columns
     ((201, 333367 // 4), (2, 1), torch.float64, 2, "deep-ring"),  # rows, odd K: element pieces
     ((200, 83336), (2, 1), torch.float64, 2, "deep-ring"),  # rows, 16-byte chunks

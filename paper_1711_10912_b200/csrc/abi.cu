@@ -48,6 +48,13 @@ int residual_enqueue(const tl_desc &a, const void *a_ptr, const double *const *u
 int ttv_describe(const tl_desc &a, int m0, char *buf, size_t len);
 int ttm_dmma_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out);
 int ttm_staged_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out);
+// ttm_few.cu: J <= 32 for any layout / mode (box of positions along A x along C)
+int ttm_few_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
+                    cudaStream_t st);
+int ttm_few_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &out);
+int ttm_few_mode();
+// ttm_simt.cu: would the stream / bulk tile kernels (first-order-compatible float64 outputs) take this ttm?
+bool ttm_tile_kernels_apply(const tl_desc &a, const tl_desc &bm, int m0);
 
 static thread_local std::string g_error = "no error";
 
@@ -261,6 +268,13 @@ static int ttm_dispatch(const tl_desc *a, const void *a_ptr, const tl_desc *bmat
     // reference's fold); anything else -> one thread per output
     const bool few_rows = bmat->extent[0] <= 32;
     const bool fp = a->dtype == TL_F64 || a->dtype == TL_F32;
+    // few rows, any layout: the box kernel, unless the tuned tile kernels
+    // (stream / bulk: first-order-compatible float64 outputs) apply
+    if (few_rows && ttm_few_mode() > 0 &&
+        (ttm_few_mode() > 1 || !ttm_tile_kernels_apply(*a, *bmat, mode - 1))) {
+        int rc = ttm_few_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st);
+        if (rc != TL_EUNSUPPORTED) return rc;
+    }
     if (few_rows || !fp) {
         int rc = ttm_staged_enqueue(*a, a_ptr, *bmat, b_ptr, c_ptr, mode - 1, st, ssq_out, ssq_ws, ssq_fused);
         if (rc != TL_EUNSUPPORTED) return rc;
@@ -450,7 +464,9 @@ int tl_plan_describe(int32_t op, const tl_desc *a, const tl_desc *bmat, int32_t 
     const bool few_rows = bmat->extent[0] <= 32;
     const bool fp = a->dtype == TL_F64 || a->dtype == TL_F32;
     int rc = TL_EUNSUPPORTED;
-    if (few_rows || !fp) rc = ttm_staged_describe(*a, *bmat, mode - 1, s);
+    if (few_rows && ttm_few_mode() > 0 && (ttm_few_mode() > 1 || !ttm_tile_kernels_apply(*a, *bmat, mode - 1)))
+        rc = ttm_few_describe(*a, *bmat, mode - 1, s);
+    if (rc == TL_EUNSUPPORTED && (few_rows || !fp)) rc = ttm_staged_describe(*a, *bmat, mode - 1, s);
     if (rc == TL_EUNSUPPORTED && fp) {
         rc = ttm_dmma_describe(*a, *bmat, mode - 1, s);
         if (rc == TL_EUNSUPPORTED && !few_rows) rc = ttm_staged_describe(*a, *bmat, mode - 1, s);

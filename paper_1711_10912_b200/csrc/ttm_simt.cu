@@ -1071,6 +1071,19 @@ int ttm_staged_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string
     return TL_OK;
 }
 
+// Would ttm_staged_enqueue run the stream or the bulk tile kernel?  (Outputs
+// are freshly allocated, so C is taken as 16-byte aligned.)
+bool ttm_tile_kernels_apply(const tl_desc &a, const tl_desc &bm, int m0) {
+    TtmSimtParams P{};
+    if (!build_params(a, (const void *)0x100000, bm, (const void *)0x200000, (void *)0x300000, m0, P)) return false;
+    if (!staged_family_ok(P, a.dtype)) return false;
+    const SmallTtmKnobs &kn = small_ttm_knobs();
+    if (!(a.dtype == TL_F64 && P.J <= 32 && P.ident && !kn.force_simt)) return false;
+    StreamPlan sp;
+    BulkPlan bp;
+    return plan_stream(P, sp) || plan_bulk(P, bp);
+}
+
 int ttm_simt_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr,
                      int m0, cudaStream_t st) {
     TtmSimtParams P{};

@@ -9,12 +9,12 @@
 //      FIRST in A's storage order (loads of one k-row are runs along A),
 //   y: `bc` consecutive values of a flattened index over the remaining digits
 //      taken in C's (first-order) order (stores are runs along C),
-// with ba * bc = 128 * NP.  The box degenerates to 1-D (bc = 1) when A's and
+// with ba * bc = 128.  The box degenerates to 1-D (bc = 1) when A's and
 // C's fastest free digits are the same dimension or C is contiguous along j.
 // Odd extents need no divisibility: x and y are flattened over whole digit
 // groups and only the last box of each group is masked.
 //
-// Each thread folds NP positions for all J rows at once (J accumulators per
+// Each thread folds one position for all J rows at once (J accumulators per
 // position, B in shared memory as [k][j]; k in order, so every output is the
 // same chain as in the other ttm kernels: fused multiply-add for float64 --
 // the DMMA semantics --, exact for float32 (products are exact in binary64)
@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "plan.h"
@@ -41,9 +42,10 @@ struct TtmFewParams {
     const void *a;
     const void *bm;
     void *c;
-    int64_t K, I, J;
+    int64_t I;
+    int32_t K, J;
     int64_t bs0, bs1, jstride;
-    int32_t ba, bc, ba_shift, bc_shift;  // box (powers of two), ba * bc = 128 * NP
+    int32_t ba, bc, ba_shift, bc_shift;  // box (powers of two), ba * bc = 128
     int32_t store;                       // FewStore
     int32_t pitch;                       // staged tile: elements per j row
     uint32_t X, Y;                       // extents of the flattened digit groups
@@ -86,10 +88,11 @@ __device__ __forceinline__ void few_decode(uint32_t x, int nd, const FastDiv *dv
     }
 }
 
-template <class T, int JB, int NP, int D>
+template <class T, int JB, int D>
 __global__ void __launch_bounds__(kFewThreads) ttm_few_kernel(const __grid_constant__ TtmFewParams P) {
     using Acc = typename AccOf<T>::type;
-    constexpr int BN = kFewThreads * NP;
+    constexpr int BN = kFewThreads;
+    constexpr int H = D / 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc *Bs = (Acc *)smem_raw;  // [K][JB], rows j >= J zero
     const size_t bbytes = ((size_t)P.K * JB * sizeof(Acc) + 15) & ~(size_t)15;
@@ -97,146 +100,347 @@ __global__ void __launch_bounds__(kFewThreads) ttm_few_kernel(const __grid_const
     int64_t *tcx = tax + P.ba;                      // [ba]
     int64_t *tay = tcx + P.ba;                      // [bc] (-1: past Y)
     int64_t *tcy = tay + P.bc;                      // [bc]
-    T *cs = (T *)(tcy + P.bc);                      // [JB][pitch] staged outputs
+    int64_t *tco = tcy + P.bc;                      // [BN] C offset of position n (-1: masked)
+    T *cs = (T *)(tco + BN);                        // ring [D][BN], then the staged outputs [JB][pitch]
 
     const int tid = threadIdx.x;
     const T *A = (const T *)P.a;
     const T *B = (const T *)P.bm;
     T *C = (T *)P.c;
-    for (int idx = tid; idx < (int)P.K * JB; idx += kFewThreads) {
+    const int J = P.J, K = P.K;
+    for (int idx = tid; idx < K * JB; idx += kFewThreads) {
         const int k = idx / JB, j = idx % JB;
-        Bs[idx] = j < P.J ? (Acc)B[j * P.bs0 + k * P.bs1] : Acc(0);
+        Bs[idx] = j < J ? (Acc)B[j * P.bs0 + k * P.bs1] : Acc(0);
     }
     uint32_t tx, ty;
     P.nx_div.divmod(blockIdx.x, ty, tx);
-    for (int t = tid; t < P.ba; t += kFewThreads) {
-        const uint64_t x = (uint64_t)tx * P.ba + t;
+    if (tid < P.ba) {
+        const uint64_t x = (uint64_t)tx * P.ba + tid;
         int64_t oa = -1, oc = 0;
         if (x < P.X) few_decode((uint32_t)x, P.nxd, P.xdiv, P.xa, P.xc, oa, oc);
-        tax[t] = oa;
-        tcx[t] = oc;
+        tax[tid] = oa;
+        tcx[tid] = oc;
     }
-    for (int t = tid; t < P.bc; t += kFewThreads) {
-        const uint64_t y = (uint64_t)ty * P.bc + t;
+    if (tid < P.bc) {
+        const uint64_t y = (uint64_t)ty * P.bc + tid;
         int64_t oa = -1, oc = 0;
         if (y < P.Y) few_decode((uint32_t)y, P.nyd, P.ydiv, P.ya, P.yc, oa, oc);
-        tay[t] = oa;
-        tcy[t] = oc;
+        tay[tid] = oa;
+        tcy[tid] = oc;
     }
     __syncthreads();
 
-    Acc acc[NP][JB];
-    const T *pa[NP];
-    bool ok[NP];
-    int xl[NP], yl[NP];
+    const int xl = tid & (P.ba - 1), yl = tid >> P.ba_shift;
+    const int64_t ax = tax[xl], ay = tay[yl];
+    const bool ok = ax >= 0 && ay >= 0;
+    // masked positions read (and discard) the tile's first valid column
+    const T *pn = A + (ok ? ax + ay : 0);
+    const int64_t I = P.I;
+    Acc acc[JB];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        const int n = tid + p * kFewThreads;
-        xl[p] = n & (P.ba - 1);
-        yl[p] = n >> P.ba_shift;
-        const int64_t ax = tax[xl[p]], ay = tay[yl[p]];
-        ok[p] = ax >= 0 && ay >= 0;
-        pa[p] = A + (ok[p] ? ax + ay : 0);
-#pragma unroll
-        for (int j = 0; j < JB; ++j) acc[p][j] = Acc(0);
-    }
-    const int64_t K = P.K, I = P.I;
-    // Each thread streams its own column(s) of A through a private ring of D
-    // k-rows in shared memory (cp.async, one group per row; only the issuing
-    // thread reads its slots, so cp.async.wait_group is the only sync): D
-    // loads per position stay in flight while the accumulators, not the
-    // operands, hold the registers.
-    {
-        T *ring = cs;  // [D][BN]; reused as the staged output tile afterwards
-        const T *pn[NP];
-#pragma unroll
-        for (int p = 0; p < NP; ++p) pn[p] = pa[p];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            if (d < K) {
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if (ok[p]) cp_async<sizeof(T)>(ring + d * BN + tid + p * kFewThreads, pn[p]);
-                    pn[p] += I;
-                }
-            }
-            cp_async_commit();
-        }
-#pragma unroll 4
-        for (int64_t k = 0; k < K; ++k) {
-            cp_async_wait<D - 1>();
-            const int slot = (int)(k & (D - 1));
-            Acc x[NP];
-#pragma unroll
-            for (int p = 0; p < NP; ++p) x[p] = ok[p] ? (Acc)ring[slot * BN + tid + p * kFewThreads] : Acc(0);
-            if (k + D < K) {
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if (ok[p]) cp_async<sizeof(T)>(ring + slot * BN + tid + p * kFewThreads, pn[p]);
-                    pn[p] += I;
-                }
-            }
-            cp_async_commit();
-            const Acc *brow = Bs + k * JB;
-#pragma unroll
-            for (int j = 0; j < JB; j += 2) {
-                Acc b0, b1;
-                few_ld2<Acc>(brow + j, b0, b1);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    acc[p][j] = few_mac(acc[p][j], x[p], b0);
-                    acc[p][j + 1] = few_mac(acc[p][j + 1], x[p], b1);
-                }
-            }
-        }
-        cp_async_wait<0>();
-    }
+    for (int j = 0; j < JB; ++j) acc[j] = Acc(0);
 
+    // Each thread streams its own column of A through a private ring in
+    // shared memory: two halves of H k-rows, one cp.async group per half (only
+    // the issuing thread reads its slots, so cp.async.wait_group is the only
+    // sync).  Up to 2H loads per position stay in flight while the
+    // accumulators, not the operands, hold the registers.
+    T *ring = cs + tid;
+    int left = K;  // rows not yet issued
+    auto issue = [&](int half) {
+        T *dst = ring + half * (H * BN);
+        if (left >= H) {
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+                cp_async<sizeof(T)>(dst + r * BN, pn);
+                pn += I;
+            }
+        } else {
+            for (int r = 0; r < left; ++r) {
+                cp_async<sizeof(T)>(dst + r * BN, pn);
+                pn += I;
+            }
+        }
+        left -= H;
+        cp_async_commit();
+    };
+    issue(0);
+    issue(1);
+    int half = 0;
+    for (int k0 = 0; k0 < K; k0 += H) {
+        cp_async_wait<1>();
+        const T *src = ring + half * (H * BN);
+        const Acc *brow = Bs + k0 * JB;
+        if (K - k0 >= H) {
+            Acc x[H];
+#pragma unroll
+            for (int r = 0; r < H; ++r) x[r] = (Acc)src[r * BN];
+            issue(half);
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+#pragma unroll
+                for (int j = 0; j < JB; j += 2) {
+                    Acc b0, b1;
+                    few_ld2<Acc>(brow + r * JB + j, b0, b1);
+                    acc[j] = few_mac(acc[j], x[r], b0);
+                    acc[j + 1] = few_mac(acc[j + 1], x[r], b1);
+                }
+            }
+        } else {
+            const int rows = K - k0;
+            for (int r = 0; r < rows; ++r) {
+                const Acc xr = (Acc)src[r * BN];
+#pragma unroll
+                for (int j = 0; j < JB; j += 2) {
+                    Acc b0, b1;
+                    few_ld2<Acc>(brow + r * JB + j, b0, b1);
+                    acc[j] = few_mac(acc[j], xr, b0);
+                    acc[j + 1] = few_mac(acc[j + 1], xr, b1);
+                }
+            }
+        }
+        half ^= 1;
+    }
+    cp_async_wait<0>();
+
+    const int64_t js = P.jstride;
     if (P.store == kFewDirect) {
         // x runs along C as well: lanes write consecutive C elements per j
+        if (!ok) return;
+        T *pc = C + tcx[xl] + tcy[yl];
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            if (!ok[p]) continue;
-            T *pc = C + tcx[xl[p]] + tcy[yl[p]];
-#pragma unroll
-            for (int j = 0; j < JB; ++j)
-                if (j < P.J) pc[j * P.jstride] = narrow<T>(acc[p][j]);
+        for (int j = 0; j < JB; ++j) {
+            if (j < J) *pc = narrow<T>(acc[j]);
+            pc += js;
         }
         return;
     }
     const int pitch = P.pitch;
     __syncthreads();  // every thread is done with its ring slots (the staged tile aliases them)
     if (P.store == kFewAlongY) {
+        {
+            T *dst = cs + yl * (P.ba + 1) + xl;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            const int pos = yl[p] * (P.ba + 1) + xl[p];
-#pragma unroll
-            for (int j = 0; j < JB; ++j) cs[j * pitch + pos] = narrow<T>(acc[p][j]);
+            for (int j = 0; j < JB; ++j) dst[j * pitch] = narrow<T>(acc[j]);
         }
         __syncthreads();
-        // y fastest: lanes write runs along C's fastest free direction
-        for (int idx = tid; idx < BN * JB; idx += kFewThreads) {
-            const int yy = idx & (P.bc - 1);
-            const int xx = (idx >> P.bc_shift) & (P.ba - 1);
-            const int j = idx / BN;
-            if (j >= P.J) break;
-            if (tax[xx] >= 0 && tay[yy] >= 0)
-                C[tcx[xx] + tcy[yy] + j * P.jstride] = cs[j * pitch + yy * (P.ba + 1) + xx];
+        // y fastest: lanes write runs along C's fastest free direction; a
+        // thread keeps one (x, y) of the box for every j
+        const int yy = tid & (P.bc - 1), xx = tid >> P.bc_shift;
+        if (tax[xx] < 0 || tay[yy] < 0) return;
+        T *pc = C + tcx[xx] + tcy[yy];
+        const T *src = cs + yy * (P.ba + 1) + xx;
+#pragma unroll
+        for (int j = 0; j < JB; ++j) {
+            if (j < J) *pc = src[j * pitch];
+            pc += js;
         }
         return;
     }
     // C contiguous along j: stage, then lanes write each position's J-run
+    tco[tid] = ok ? tcx[xl] + tcy[yl] : -1;
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        const int n = tid + p * kFewThreads;
+    for (int j = 0; j < JB; ++j) cs[j * pitch + tid] = narrow<T>(acc[j]);
+    __syncthreads();
+    {
+        const int j = tid % JB;
+        if (j >= J) return;
+        const T *src = cs + j * pitch;
+#pragma unroll 4
+        for (int n = tid / JB; n < BN; n += kFewThreads / JB) {
+            const int64_t co = tco[n];
+            if (co >= 0) C[co + j] = src[n];
+        }
+    }
+}
+
+// ---------------------------------------------------- float64 / float32: DMMA
+// The SIMT fold above reads every b(j, k) from shared memory for every
+// position (8 broadcast LDS.128 per k-row and warp: measured bound by the
+// shared-memory data pipe at ~0.55 of HBM).  On the FP64 tensor cores
+// (mma.sync.m16n8k4.f64 -> DMMA.8x8x4, k in order = the same FMA chain) the
+// matrix fragment is 2 doubles per lane and k-step, shared by the warp's four
+// n8 tiles: 6 LDS.64 per 4 k-rows instead of 36 LDS.  Each warp owns 32
+// positions (4 n8 tiles) of the box; its lanes fill the ring columns of those
+// 32 positions (cp.async, zero-filled past K) and read fragments across lanes
+// (__syncwarp after the group wait).  float32 operands are widened on the
+// fragment loads (exact products).
+constexpr int kFewRingPitch = kFewThreads + 4;  // = 4 mod 16: conflict-free fragment loads
+
+__host__ __device__ __forceinline__ int few_ldb(int K) {
+    int l = (K + 3) / 4 * 4;
+    while (l % 16 != 4) l += 4;
+    return l;
+}
+
+__device__ __forceinline__ void few_mma(double (&d)[4], double a0, double a1, double b) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+                 : "d"(a0), "d"(a1), "d"(b));
+}
+
+template <class T> __device__ __forceinline__ void few_cp_zfill(void *smem_dst, const void *gmem_src, bool valid) {
+    const int n = valid ? (int)sizeof(T) : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src),
+                 "n"((int)sizeof(T)), "r"(n));
+}
+
+template <class T, int MT, int D>
+__global__ void __launch_bounds__(kFewThreads) ttm_few_dmma_kernel(const __grid_constant__ TtmFewParams P) {
+    constexpr int BN = kFewThreads, H = D / 2, RP = kFewRingPitch, JB = 16 * MT;
+    static_assert(H % 4 == 0, "whole k-steps per ring half");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int J = P.J, K = P.K;
+    const int ldb = few_ldb(K);
+    double *Bm = (double *)smem_raw;  // [JB][ldb], zero padded in j and k
+    int64_t *tax = (int64_t *)(Bm + JB * ldb);
+    int64_t *tcx = tax + P.ba;
+    int64_t *tay = tcx + P.ba;
+    int64_t *tcy = tay + P.bc;
+    int64_t *tco = tcy + P.bc;  // [BN]
+    T *cs = (T *)(tco + BN);    // ring [D][RP], then the staged outputs [JB][pitch]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const T *A = (const T *)P.a;
+    const T *B = (const T *)P.bm;
+    T *C = (T *)P.c;
+    uint32_t tx, ty;
+    P.nx_div.divmod(blockIdx.x, ty, tx);
+    // this thread's own column first (registers only), so its loads are in
+    // flight while the matrix image and the box tables are built
+    const int xl = tid & (P.ba - 1), yl = tid >> P.ba_shift;
+    int64_t ax = -1, cx = 0, ay = -1, cy = 0;
+    {
+        const uint64_t x = (uint64_t)tx * P.ba + xl, y = (uint64_t)ty * P.bc + yl;
+        if (x < P.X) few_decode((uint32_t)x, P.nxd, P.xdiv, P.xa, P.xc, ax, cx);
+        if (y < P.Y) few_decode((uint32_t)y, P.nyd, P.ydiv, P.ya, P.yc, ay, cy);
+    }
+    const bool ok = ax >= 0 && ay >= 0;
+    const T *pn = A + (ok ? ax + ay : 0);  // masked positions read (and discard) column 0
+    const int64_t I = P.I;
+    double acc[MT][4][4];
 #pragma unroll
-        for (int j = 0; j < JB; ++j) cs[j * pitch + n] = narrow<T>(acc[p][j]);
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][n][v] = 0.0;
+
+    T *ring = cs + tid;  // this thread's column
+    int left = K;        // rows not yet issued
+    auto issue = [&](int half) {
+        T *dst = ring + half * (H * RP);
+        if (left >= H) {
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+                cp_async<sizeof(T)>(dst + r * RP, pn);
+                pn += I;
+            }
+        } else if (left > 0) {
+            // last rows, zero-filled up to a whole k-step
+            const int upto = (left + 3) & ~3;
+            for (int r = 0; r < upto; ++r) {
+                few_cp_zfill<T>(dst + r * RP, r < left ? pn : A, r < left);
+                if (r < left) pn += I;
+            }
+        }
+        left -= H;
+        cp_async_commit();
+    };
+    issue(0);
+    issue(1);
+    for (int m = warp; m < JB; m += kFewThreads / 32)
+        for (int k = lane; k < ldb; k += 32) Bm[m * ldb + k] = (m < J && k < K) ? (double)B[m * P.bs0 + k * P.bs1] : 0.0;
+    if (tid < P.ba) {
+        tax[tid] = ax;
+        tcx[tid] = cx;
+    }
+    if (tid < P.bc) {
+        const uint64_t y = (uint64_t)ty * P.bc + tid;
+        int64_t oa = -1, oc = 0;
+        if (y < P.Y) few_decode((uint32_t)y, P.nyd, P.ydiv, P.ya, P.yc, oa, oc);
+        tay[tid] = oa;
+        tcy[tid] = oc;
     }
     __syncthreads();
-    for (int idx = tid; idx < BN * JB; idx += kFewThreads) {
-        const int j = idx % JB, n = idx / JB;
-        const int xx = n & (P.ba - 1), yy = n >> P.ba_shift;
-        if (j < P.J && tax[xx] >= 0 && tay[yy] >= 0) C[tcx[xx] + tcy[yy] + j] = cs[j * pitch + n];
+    int half = 0;
+    const T *frag = cs + warp * 32 + g;  // + (k row) * RP + n8 tile * 8
+    for (int k0 = 0; k0 < K; k0 += H) {
+        cp_async_wait<1>();
+        __syncwarp();
+        const T *src = frag + half * (H * RP);
+        double bf[H / 4][4];
+#pragma unroll
+        for (int s = 0; s < H / 4; ++s)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) bf[s][n] = (k0 + 4 * s < K) ? (double)src[(4 * s + t) * RP + n * 8] : 0.0;
+        __syncwarp();  // every lane holds its fragments: the half can be refilled
+        issue(half);
+#pragma unroll
+        for (int s = 0; s < H / 4; ++s) {
+            if (k0 + 4 * s < K) {
+                const double *bm = Bm + g * ldb + k0 + 4 * s + t;
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const double a0 = bm[(16 * i) * ldb], a1 = bm[(16 * i + 8) * ldb];
+#pragma unroll
+                    for (int n = 0; n < 4; ++n) few_mma(acc[i][n], a0, a1, bf[s][n]);
+                }
+            }
+        }
+        half ^= 1;
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // every warp is done with the ring (the staged tile aliases it)
+
+    // fragments -> staged tile cs[j][pos]: row j = 16 i + g + 8 h, column n = 32 warp + 8 n8 + 2 t + v
+    const int pitch = P.pitch;
+    const bool along_y = P.store == kFewAlongY;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const int col = warp * 32 + n * 8 + 2 * t + v;
+            const int pos = along_y ? (col >> P.ba_shift) * (P.ba + 1) + (col & (P.ba - 1)) : col;
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) cs[(16 * i + g + 8 * h) * pitch + pos] = (T)acc[i][n][2 * h + v];
+        }
+    }
+    if (P.store == kFewAlongJ) tco[tid] = ok ? cx + cy : -1;
+    __syncthreads();
+    const int64_t js = P.jstride;
+    if (P.store != kFewAlongJ) {
+        // a thread keeps one position of the box for every j: lanes along y
+        // (C's fastest free direction) or, for direct boxes, along x
+        int xx = xl, yy = yl, pos = tid;
+        if (along_y) {
+            yy = tid & (P.bc - 1);
+            xx = tid >> P.bc_shift;
+            pos = yy * (P.ba + 1) + xx;
+        }
+        if (tax[xx] < 0 || tay[yy] < 0) return;
+        T *pc = C + tcx[xx] + tcy[yy];
+        const T *src = cs + pos;
+#pragma unroll
+        for (int j = 0; j < JB; ++j) {
+            if (j < J) *pc = src[j * pitch];
+            pc += js;
+        }
+        return;
+    }
+    {
+        // C contiguous along j: lanes write each position's J-run
+        const int j = tid % JB;
+        if (j >= J) return;
+        const T *src = cs + j * pitch;
+#pragma unroll 4
+        for (int n = tid / JB; n < BN; n += kFewThreads / JB) {
+            const int64_t co = tco[n];
+            if (co >= 0) C[co + j] = src[n];
+        }
     }
 }
 
@@ -247,7 +451,8 @@ struct FewDigit {
 
 struct FewPlan {
     TtmFewParams P{};
-    int jb = 0, np = 0;
+    int jb = 0, mt = 1;
+    bool dmma = false;
     size_t smem = 0;
     int64_t grid = 0;
 };
@@ -278,15 +483,15 @@ static bool plan_few(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     const int64_t F = cn.O * cn.I;
     if (F < 1 || F > kIdx32 || cn.K > (1 << 20)) return false;
     const int jb = J <= 4 ? 4 : J <= 8 ? 8 : J <= 16 ? 16 : 32;
-    // positions per thread (TL_TTM_FEW_NP; measured: DESIGN.md)
-    static const int np_knob = [] {
-        const char *e = getenv("TL_TTM_FEW_NP");
-        return e ? atoi(e) : 1;
-    }();
-    const int np = (jb <= 16 && np_knob == 2) ? 2 : 1;
-    const int BN = kFewThreads * np;
-    const size_t bbytes = ((size_t)cn.K * jb * 8 + 15) & ~(size_t)15;
-    if (bbytes > 64 * 1024) return false;
+    const int BN = kFewThreads;
+    // long folds: the GETT's k-tiled operands (no whole-matrix image per CTA)
+    if (cn.K > 128 && J >= 8 && a.dtype != TL_I64) return false;
+    // FP64 tensor cores from K = 9 (measured: below, the SIMT fold's smaller
+    // fixed cost per box wins; both fold k in order with fused multiply-adds)
+    const bool dmma = a.dtype != TL_I64 && cn.K > 8;
+    const int mt = J <= 16 ? 1 : 2;
+    const size_t bbytes = dmma ? (size_t)16 * mt * few_ldb((int)cn.K) * 8 : (((size_t)cn.K * jb * 8 + 15) & ~(size_t)15);
+    if (bbytes > 96 * 1024) return false;
     // free digits in A order with A strides
     std::vector<FewDigit> dg;
     {
@@ -339,9 +544,9 @@ static bool plan_few(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     P.a = (const unsigned char *)a_ptr + a.offset * es;
     P.bm = (const unsigned char *)b_ptr + bm.offset * es;
     P.c = c_ptr;
-    P.K = cn.K;
+    P.K = (int32_t)cn.K;
     P.I = cn.I;
-    P.J = J;
+    P.J = (int32_t)J;
     P.bs0 = bm.stride[0];
     P.bs1 = bm.stride[1];
     P.jstride = cn.jstride;
@@ -377,13 +582,15 @@ static bool plan_few(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     if (nX * nY > 0x7fffffffll) return false;
     P.nx_div.init((uint32_t)nX);
     P.pitch = store == kFewAlongY ? bc * (ba + 1) : BN + 1;
+    if (dmma) P.pitch = (P.pitch + 3) / 4 * 4 + 1;  // odd pitch: the fragment rows g, g + 8 spread over the banks
     fp.jb = jb;
-    fp.np = np;
+    fp.dmma = dmma;
+    fp.mt = mt;
     fp.grid = nX * nY;
-    const size_t ring = (size_t)kFewRing * BN * es;
-    const size_t stage = store == kFewDirect ? 0 : (size_t)jb * P.pitch * es;
-    fp.smem = bbytes + (size_t)2 * (ba + bc) * 8 + std::max(ring, stage);
-    return fp.smem <= 160 * 1024;
+    const size_t ring = (size_t)kFewRing * (dmma ? kFewRingPitch : BN) * es;
+    const size_t stage = dmma ? (size_t)16 * mt * P.pitch * es : (store == kFewDirect ? 0 : (size_t)jb * P.pitch * es);
+    fp.smem = bbytes + (size_t)2 * (ba + bc) * 8 + (size_t)BN * 8 + std::max(ring, stage);
+    return fp.smem <= 150 * 1024;
 }
 
 template <class T> static int few_launch(const FewPlan &fp, cudaStream_t st) {
@@ -393,18 +600,14 @@ template <class T> static int few_launch(const FewPlan &fp, cudaStream_t st) {
         kern<<<(unsigned)fp.grid, kFewThreads, fp.smem, st>>>(fp.P);
         return cuda_status(cudaGetLastError(), "ttm few launch");
     };
-    if (fp.np == 2) {
-        switch (fp.jb) {
-            case 4: return go(ttm_few_kernel<T, 4, 2, kFewRing>);
-            case 8: return go(ttm_few_kernel<T, 8, 2, kFewRing>);
-            default: return go(ttm_few_kernel<T, 16, 2, kFewRing>);
-        }
+    if constexpr (!std::is_same<T, int64_t>::value) {
+        if (fp.dmma) return fp.mt == 1 ? go(ttm_few_dmma_kernel<T, 1, kFewRing>) : go(ttm_few_dmma_kernel<T, 2, kFewRing>);
     }
     switch (fp.jb) {
-        case 4: return go(ttm_few_kernel<T, 4, 1, kFewRing>);
-        case 8: return go(ttm_few_kernel<T, 8, 1, kFewRing>);
-        case 16: return go(ttm_few_kernel<T, 16, 1, kFewRing>);
-        default: return go(ttm_few_kernel<T, 32, 1, kFewRing>);
+        case 4: return go(ttm_few_kernel<T, 4, kFewRing>);
+        case 8: return go(ttm_few_kernel<T, 8, kFewRing>);
+        case 16: return go(ttm_few_kernel<T, 16, kFewRing>);
+        default: return go(ttm_few_kernel<T, 32, kFewRing>);
     }
 }
 

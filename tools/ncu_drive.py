@@ -60,6 +60,19 @@ def main(which):
             keep.append(C2n)
             ops.append(lambda C2n=C2n: C.frobenius_norm_device(C2n))
             del T
+    if "few" in which:
+        # few-row ttm (J = 16) on the config-5 ttm operand shape: first-order modes
+        # 4 / 5 (direct stores), a permuted layout's modes 1 (along j), 2 and 5 (boxes)
+        import numpy as np
+        from paper_1711_10912_b200.layout import TensorMeta
+        shape = (3, 33, 5, 17, 2, 640)
+        A0 = tl.DenseTensor._wrap(TensorMeta(shape), torch.rand(int(np.prod(shape)), dtype=torch.float64, device="cuda"))
+        Ap = tl.DenseTensor._wrap(TensorMeta(shape), A0.buffer.clone())
+        Ap.relayout((4, 3, 6, 5, 1, 2))
+        Ms = [tl.DenseTensor._wrap(TensorMeta((16, n)), torch.randn(16 * n, dtype=torch.float64, device="cuda")) for n in shape]
+        keep += [A0, Ap, Ms]
+        for A, m in ((A0, 4), (A0, 5), (Ap, 1), (Ap, 2), (Ap, 5)):
+            ops.append(lambda A=A, m=m: tl.ttm(A, Ms[m - 1], m))
     if "copy" in which:
         # relayout / transpose kernels on the config-2 tensor (first -> last,
         # first -> seeded permutation, first -> (2,1,3,4))

@@ -517,24 +517,30 @@ static bool plan_few(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
         store = cn.jstride == 1 ? kFewAlongJ : kFewDirect;
     } else {
         // x: A's fastest digits up to (not including) C's fastest digit, until
-        // they span >= 16 positions; y: the rest in C order
+        // they span the box width with few masked lanes (an extent such as 17
+        // alone would waste 41% of a width-8 box: flattening the next digit
+        // into x removes the ragged edge); y: the rest in C order
+        // Box width along x by the traffic mix: the output is J/K of the
+        // input, so a short fold wants long runs along C (wide in y; a 32-byte
+        // sector along A is enough, L1 keeps its other half for the next
+        // k-rows) and a long fold long runs along A.
+        const int target = cn.K >= 2 * J ? 32 : cn.K >= J ? 16 : 2 * cn.K >= J ? 8 : 4;
+        auto pick = [&](int64_t X, int &b) {
+            if (X <= target) {
+                b = 2;
+                while (b < X) b *= 2;
+                return (double)b / (double)X;
+            }
+            b = target;
+            return (double)((X + b - 1) / b * b) / (double)X;
+        };
         int64_t X = 1;
         size_t r = 0;
-        while (r < ic && X < 16) X *= dg[r++].ext;
+        while (r < ic && (X < target || pick(X, ba) > 1.15)) X *= dg[r++].ext;
+        pick(X, ba);
         gx.assign(dg.begin(), dg.begin() + r);
         gy.assign(dg.begin() + r, dg.end());
         std::stable_sort(gy.begin(), gy.end(), [](const FewDigit &p, const FewDigit &q) { return p.cs < q.cs; });
-        // box width along x: the power of two in [2, 32] with the least masked
-        // lanes in the last box (ties: 16, then wider)
-        const int cand[5] = {16, 32, 8, 4, 2};
-        double best = 1e30;
-        for (int b : cand) {
-            const double waste = (double)((X + b - 1) / b * b) / (double)X;
-            if (waste < best - 1e-9) {
-                best = waste;
-                ba = b;
-            }
-        }
         bc = BN / ba;
         store = kFewAlongY;
     }

@@ -557,6 +557,34 @@ def components(args, wl=None):
         }
         del A, C1, C2
         torch.cuda.empty_cache()
+    # north_star "across all layouts and modes": the config-5 ttm operand shape
+    # (3,33,5,17,2,640) x a 16-row matrix in the first-order and three seeded
+    # permutation layouts, every mode (24 ttms; the full tables over all configs
+    # are tools/experiments/config_sweep.py -> profiles/config_sweep_*.md)
+    from paper_1711_10912_b200.layout import TensorMeta
+    shape5 = (3, 33, 5, 17, 2, 640)
+    n5m = int(np.prod(shape5))
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A0 = tl.DenseTensor._wrap(TensorMeta(shape5), torch.rand(n5m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1)
+    Ms = [tl.DenseTensor._wrap(TensorMeta((16, k)), torch.randn(16 * k, dtype=torch.float64, device="cuda", generator=g))
+          for k in shape5]
+    refs = [tl.ttm(A0, Ms[m], m + 1).buffer.clone() for m in range(6)]
+    fr, same = [], True
+    for lay in [tuple(range(1, 7))] + [W.random_layout(6, sd) for sd in (0, 1, 2)]:
+        Ap = tl.DenseTensor._wrap(TensorMeta(shape5), A0.buffer.clone())
+        Ap.relayout(lay)
+        for m in range(6):
+            same = same and bool(torch.equal(tl.ttm(Ap, Ms[m], m + 1).buffer, refs[m]))
+            t = med(lambda: tl.ttm(Ap, Ms[m], m + 1), iters=3, warm=1, reps=5)
+            nb = 8 * (n5m + 16 * shape5[m] + n5m // shape5[m] * 16)
+            fr.append(nb / (t * 1e-3) / 1e9 / peak)
+        del Ap
+    fr.sort()
+    out["cfg5_ttm_every_layout_mode"] = {"cases": len(fr), "frac_hbm_min": round(fr[0], 3),
+                                         "frac_hbm_median": round(fr[len(fr) // 2], 3), "frac_hbm_max": round(fr[-1], 3),
+                                         "bit_identical_across_layouts": same}
+    del A0, Ms, refs
+    torch.cuda.empty_cache()
     return out
 
 

@@ -100,6 +100,8 @@ struct ReduceParams {
     int64_t init_i;
     int64_t n_rows, row_len;  // dot_rows
     DigitMap rows_a, rows_b;  // row index -> element offsets
+    int32_t row_vec;          // rows are whole, aligned 16-byte vectors in both operands
+    FastDiv rowv_div;         // vectors per row
     // dot_tiled
     int64_t nX, nY, n_rest;
     int64_t a_sY, b_sX;  // a's stride along Y, b's stride along X
@@ -275,6 +277,44 @@ __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ R
             }
         }
         for (int64_t e = nv * VEC + tid; e < L; e += nthreads) ta.add(0, as_acc(a[e]), as_acc(b[e]));
+    } else if (VEC > 1 && P.row_vec) {
+        // rows along the shared fastest dimension, in a different order in b
+        // (e.g. layouts (1,2,3,4) x (1,4,2,3)): 16-byte vectors, U in flight
+        // per thread and operand, row starts through b's digit map
+        const uint32_t nvr = (uint32_t)(L / VEC);
+        const int64_t nv = P.n_rows * nvr;
+        auto offs = [&](int64_t v, int64_t &oa, int64_t &ob) {
+            uint32_t r, c;
+            P.rowv_div.divmod((uint32_t)v, r, c);
+            oa = (int64_t)r * L + (int64_t)c * VEC;
+            ob = P.rows_b.map(r) + (int64_t)c * VEC;
+        };
+        int64_t v = tid;
+        for (; v + (U - 1) * nthreads < nv; v += U * nthreads) {
+            TA xa[U][VEC];
+            TB xb[U][VEC];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                int64_t oa, ob;
+                offs(v + u * nthreads, oa, ob);
+                load_vec<TA, VEC>(a + oa, xa[u]);
+                load_vec<TB, VEC>(b + ob, xb[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) ta.add(u * VEC + j, as_acc(xa[u][j]), as_acc(xb[u][j]));
+        }
+        for (; v < nv; v += nthreads) {
+            TA xa[VEC];
+            TB xb[VEC];
+            int64_t oa, ob;
+            offs(v, oa, ob);
+            load_vec<TA, VEC>(a + oa, xa);
+            load_vec<TB, VEC>(b + ob, xb);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) ta.add(j, as_acc(xa[j]), as_acc(xb[j]));
+        }
     } else {
         const int64_t total = P.n_rows * L;
         for (int64_t e = tid; e < total; e += nthreads) {
@@ -666,6 +706,15 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         const uintptr_t pa = (uintptr_t)P.a, pb = (uintptr_t)P.b;
         const bool same = (P.a == P.b) && (a.dtype == b.dtype) && P.n_rows == 1;
         const bool al = (pa % 16 == 0 && pb % 16 == 0);
+        if (P.n_rows > 1 && al && a.dtype == b.dtype) {
+            const int64_t V = 16 / (int64_t)sa;
+            bool ok = row_len % V == 0 && N / V <= 0xffffffffll;
+            for (auto &dg : rb) ok = ok && dg.second % V == 0;
+            if (ok) {
+                P.row_vec = 1;
+                P.rowv_div.init((uint32_t)(row_len / V));
+            }
+        }
         const unsigned G = (unsigned)grid;
         if (a.dtype == TL_F32 && b.dtype == TL_F32) {
             if (same && al) dot_rows_kernel<float, float, 4, true, 8><<<G, threads, 0, st>>>(P);  // 8 x 16 B in flight: one stream

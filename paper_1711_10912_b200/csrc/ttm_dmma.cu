@@ -61,6 +61,9 @@ using Tile4 = GettTile<128, 64, 32, 2>;
 using Tile9 = GettTile<64, 64, 32, 2>;
 using Tile10 = GettTile<64, 64, 16, 3>;
 using Tile12 = GettTile<64, 64, 16, 2>;
+// few rows (J <= 16 / <= 32, long folds): no idle MMA rows, 128 free positions per CTA
+using Tile16 = GettTile<16, 128, 32, 2>;
+using Tile32 = GettTile<32, 128, 32, 2>;
 
 // warp layout: WM x WN warps, each TM m16 tiles x TN n8 tiles
 template <int WM_, int WN_, int TM_, int TN_> struct GettCfg {
@@ -70,6 +73,8 @@ template <int WM_, int WN_, int TM_, int TN_> struct GettCfg {
 using Cfg16 = GettCfg<4, 4, 2, 4>;  // Tile1: 16 warps of 32 x 32
 using Cfg8x = GettCfg<4, 2, 2, 4>;  // Tile4: 8 warps of 32 x 32
 using Cfg4y = GettCfg<2, 2, 2, 4>;  // Tile9/10: 4 warps of 32 x 32
+using Cfg16n = GettCfg<1, 4, 1, 4>;  // Tile16: 4 warps of 16 x 32
+using Cfg32n = GettCfg<1, 4, 2, 4>;  // Tile32: 4 warps of 32 x 32
 
 struct TtmParams {
     const void *a;  // TA elements (float64, or float32 widened exactly on the fragment loads)
@@ -412,14 +417,20 @@ int ttm_dmma_describe(const tl_desc &a, const tl_desc &bm, int m0, std::string &
 static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, const void *b_ptr, void *c_ptr, int m0,
                     cudaStream_t st, std::string *describe) {
     // CTA tile (see the table above Tile1); TL_GETT_TILE = 1, 4, 9 or 10
-    static const int tile_kind = [] {
+    static const int tile_env = [] {
         const char *e = getenv("TL_GETT_TILE");
         const int k = e ? atoi(e) : 9;
         return (k == 1 || k == 4 || k == 10 || k == 12) ? k : 9;
     }();
-    const int BM = tile_kind >= 9 ? 64 : 128;
-    const int BN = tile_kind == 1 ? 128 : 64;
+    static const bool few_tiles = [] {
+        const char *e = getenv("TL_GETT_FEW");
+        return e ? atoi(e) != 0 : true;
+    }();
     const int64_t J = bm.extent[0];
+    // few rows (reached for long folds, K > 128): a 16- or 32-row tile instead of 64 rows of mostly idle MMAs
+    const int tile_kind = (few_tiles && a.dtype == TL_F64 && J <= 32) ? (J <= 16 ? 16 : 32) : tile_env;
+    const int BM = tile_kind == 16 ? 16 : tile_kind == 32 ? 32 : tile_kind >= 9 ? 64 : 128;
+    const int BN = (tile_kind == 1 || tile_kind == 16 || tile_kind == 32) ? 128 : 64;
     Canon cn;
     if (!canon_contraction(a, m0, J, cn)) {
         set_error("ttm: operand A is not a dense permutation layout (materialise views first)");
@@ -567,6 +578,8 @@ static int gett_run(const tl_desc &a, const void *a_ptr, const tl_desc &bm, cons
                         : go(ttm_dmma_kernel<TA, CFG, TL, false, false, false, MINB>);
     };
     if (f32) return launch(float{}, Cfg4y{}, Tile9{}, std::integral_constant<int, 3>{});
+    if (tile_kind == 16) return launch(double{}, Cfg16n{}, Tile16{}, std::integral_constant<int, 2>{});
+    if (tile_kind == 32) return launch(double{}, Cfg32n{}, Tile32{}, std::integral_constant<int, 2>{});
     if (tile_kind == 1) return launch(double{}, Cfg16{}, Tile1{}, std::integral_constant<int, 1>{});
     if (tile_kind == 4) return launch(double{}, Cfg8x{}, Tile4{}, std::integral_constant<int, 2>{});
     if (tile_kind == 10) return launch(double{}, Cfg4y{}, Tile10{}, std::integral_constant<int, 3>{});

@@ -20,6 +20,10 @@ tools/ncu_box.sh prof_red "dot_" cfg2
 tools/ncu_box.sh prof_hopm "ttv_" cfg4
 tools/ncu_box.sh prof_cfg5 "ttv_|ttm_|dot_" cfg5
 tools/ncu_box.sh prof_copy "copy" copy
+tools/ncu_box.sh prof_few "ttm_few" few
+# every layout x every mode of the configs' shapes (profiles/config_sweep_<tag>.md via tools/summarize_sweep.py)
+timeout 1200 python tools/experiments/config_sweep.py ttv2,ttv4,ttv5,ttm3,ttm5,inner 8 > gpurun_out/config_sweep.jsonl 2> gpurun_out/config_sweep.err
+TL_TTM_FEW=0 timeout 600 python tools/experiments/config_sweep.py ttm5 8 > gpurun_out/config_sweep_ttm5_before.jsonl 2>> gpurun_out/config_sweep.err
 tools/experiments/hopm_dram.sh
 rm -f gpurun_out/*.ncu-rep
 du -sh gpurun_out

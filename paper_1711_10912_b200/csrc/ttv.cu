@@ -1383,6 +1383,12 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
         while (R > 1 && (O + R - 1) / R < nsm && R * I > 64) R /= 2;
         threads = (int)std::min<int64_t>(256, std::max<int64_t>(32, ((R * I + 31) / 32) * 32));
     }
+    // (rows of a few elements are padded to a bank-friendly pitch, e.g. 6 -> 18
+    // doubles: when the padded stages overflow shared memory, halve the rows
+    // per tile instead of giving the tensor to the strided kernel, whose
+    // one-thread-per-fibre walk over I < 32 measured 0.08-0.17 of HBM)
+    for (;; R /= 2) {
+    if (I != 1) threads = (int)std::min<int64_t>(256, std::max<int64_t>(32, ((R * I + 31) / 32) * 32));
     // piece size: must divide the global row pitch and the base address
     int64_t G = 16;
     while (G > (int64_t)s && (((K * I * s) % G) != 0 || (base_addr % G) != 0)) G /= 2;
@@ -1422,7 +1428,12 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     const int64_t bbytes = ((K * 8) + 15) & ~15ll;
     const int64_t stage_bytes = ((R * Lp * s) + 15) & ~15ll;
     const int64_t smem = bbytes + kStages * stage_bytes;
-    if (smem > 200 * 1024) return false;
+    if (smem > 200 * 1024) {
+        // (only for I <= 8: from there the strided kernel's fibres are long
+        // enough, I = 15: 191 vs 246 us staged)
+        if (I != 1 && I <= 8 && R >= 2 && R * I > 64) continue;
+        return false;
+    }
     // contiguous-chunk mode: one slab, no padding -> 1-D TMA bulk copies
     L.bulk = (Kc == K) && (Lp == L0) && (base_addr % 16 == 0) && ((R * K * I * s) % 16 == 0);
     P.R = (int32_t)R;
@@ -1446,6 +1457,7 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     const int64_t grid = std::min<int64_t>(P.ntiles, (int64_t)nsm * per_sm);
     L.grid = dim3((unsigned)grid);
     return true;
+    }
 }
 
 static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, int32_t a_dtype) {
@@ -1477,7 +1489,10 @@ static bool plan_strided(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm, 
     }();
     // scramble only slabs of up to 256 KB (larger ones, e.g. HOPM's 1.28 MB,
     // measure slightly better in storage order)
-    int64_t m = (P.K * P.I * s <= (256 << 10)) ? omul_env : 1;
+    // ... and not slabs of under 1 KB: consecutive threads then belong to
+    // consecutive slabs, and visiting those 257 apart scatters every warp's
+    // loads and stores over isolated sectors (K = 3, I = 2: 0.08 of HBM)
+    int64_t m = (P.K * P.I * s <= (256 << 10) && P.K * P.I * s >= 1024) ? omul_env : 1;
     while (m > 1 && std::gcd(m, P.O) != 1) m += 2;
     P.o_mul = (P.O > 1 && m > 1) ? m % P.O : 1;
     if (P.o_mul == 0) P.o_mul = 1;

@@ -158,18 +158,26 @@ def test_ttm_small_j_plans():
     p = plan(1, (5, 37, 20001), (1, 2, 3), 2, _abi.TL_F64, (32, 37))
     assert p["path"] == "stream" and p["warps"] == 8 and p["slots_per_warp"] >= 2
     assert (p["R"] * p["I"]) <= 8 * p["NT"] and p["R"] * p["K"] * p["I"] % 2 == 0
-    # no stream plan (R*I = 256 positions exceed a warp) and a bulk plan would
-    # need 512 threads for its 256-thread kernel -> the staged kernel (the
-    # wide-fuzz regression, tests/test_gpu_api.py)
+    # Where the stream / bulk tile kernels do not apply (R*I = 256 positions
+    # exceed a warp and a bulk plan would need 512 threads: the wide-fuzz
+    # regression; permuted outputs; float32 / int64), the few-row box kernel
+    # of csrc/ttm_few.cu takes J <= 32 with K <= 128 (round 2)
     p = plan(1, (2, 8, 16, 7, 5, 2, 8), (1, 2, 3, 4, 5, 6, 7), 4, _abi.TL_F64, (25, 7))
-    assert (p["path"], p["I"]) == ("staged", 256)
-    # permuted outputs (not in A's order) and float32/int64 go to the staged kernel
-    assert plan(1, (20, 60, 3), (2, 1, 3), 1, _abi.TL_F64, (32, 20))["path"] == "staged"
-    # a B image past 48 KB (J * K = 32 * 200) leaves the family -> GETT
+    assert (p["path"], p["store"], p["ba"] * p["bc"]) == ("few", "direct", 128)
+    # permuted output whose fastest free digit differs from A's: a 2-D box written along C
+    p = plan(1, (20, 60, 3), (2, 1, 3), 1, _abi.TL_F64, (32, 20))
+    assert (p["path"], p["store"]) == ("few", "along-j")  # mode 1: C is contiguous along j
+    p = plan(1, (3, 33, 5, 17, 2, 640), (4, 3, 6, 5, 1, 2), 2, _abi.TL_F64, (16, 33))
+    assert (p["path"], p["store"], p["ba"] * p["bc"]) == ("few", "along-y", 128)
+    assert p["X"] * p["Y"] == 3 * 5 * 17 * 2 * 640 and p["ba"] == 32  # K >= 2 J: long runs along A
+    p = plan(1, (3, 33, 5, 17, 2, 640), (4, 3, 6, 5, 1, 2), 5, _abi.TL_F64, (16, 2))
+    assert (p["path"], p["store"], p["ba"]) == ("few", "along-y", 4)  # K < J / 2: long runs along C
+    # long folds (K > 128) keep the GETT, now with a 16- / 32-row tile
     assert plan(1, (200, 60, 3), (2, 1, 3), 1, _abi.TL_F64, (32, 200))["path"] == "gett"
-    assert plan(1, (3, 33, 5, 17), (1, 2, 3, 4), 2, _abi.TL_F32, (16, 33))["path"] == "staged"
-    # I > 256: outside the staged family -> GETT (J >= 8, GEMM-shaped) or SIMT
-    assert plan(1, (9, 31, 4), (1, 2, 3), 3, _abi.TL_F64, (15, 4))["path"] == "simt"
+    assert plan(1, (3, 33, 5, 17), (1, 2, 3, 4), 2, _abi.TL_F32, (16, 33))["path"] == "few"
+    assert plan(1, (9, 31, 4), (1, 2, 3), 3, _abi.TL_F64, (15, 4))["path"] == "few"
+    # more than 32 rows: GETT / staged / SIMT as before
+    assert plan(1, (9, 31, 4), (1, 2, 3), 3, _abi.TL_F64, (40, 4))["path"] == "simt"
 
 
 def test_compute_strides_rule_and_erratum():

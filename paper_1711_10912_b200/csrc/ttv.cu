@@ -1429,9 +1429,11 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     const int64_t stage_bytes = ((R * Lp * s) + 15) & ~15ll;
     const int64_t smem = bbytes + kStages * stage_bytes;
     if (smem > 200 * 1024) {
-        // (only for I <= 8: from there the strided kernel's fibres are long
-        // enough, I = 15: 191 vs 246 us staged)
-        if (I != 1 && I <= 8 && R >= 2 && R * I > 64) continue;
+        // (only for I <= 4, or I <= 8 with slabs of 4 KB and more, where the
+        // strided kernel's per-thread streams thrash DRAM pages: K = 640, I = 6
+        // 326 -> 270 us; short slabs with I = 5..6 measured better strided,
+        // K = 17, I = 5: 191 vs 246 us)
+        if (I != 1 && (I <= 4 || (I <= 8 && K * I * s >= 4096)) && R >= 2 && R * I > 64) continue;
         return false;
     }
     // contiguous-chunk mode: one slab, no padding -> 1-D TMA bulk copies

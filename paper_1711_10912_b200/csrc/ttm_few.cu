@@ -50,6 +50,7 @@ struct TtmFewParams {
     int32_t pitch;                       // staged tile: elements per j row
     uint32_t X, Y;                       // extents of the flattened digit groups
     FastDiv nx_div;                      // tile -> (x box, y box), x fastest
+    uint32_t ntiles;
     int32_t nxd, nyd;
     FastDiv xdiv[TL_MAX_DIGITS], ydiv[TL_MAX_DIGITS];
     int64_t xa[TL_MAX_DIGITS], xc[TL_MAX_DIGITS], ya[TL_MAX_DIGITS], yc[TL_MAX_DIGITS];
@@ -293,42 +294,42 @@ __global__ void __launch_bounds__(kFewThreads) ttm_few_dmma_kernel(const __grid_
     const int J = P.J, K = P.K;
     const int ldb = few_ldb(K);
     double *Bm = (double *)smem_raw;  // [JB][ldb], zero padded in j and k
-    int64_t *tax = (int64_t *)(Bm + JB * ldb);
-    int64_t *tcx = tax + P.ba;
-    int64_t *tay = tcx + P.ba;
-    int64_t *tcy = tay + P.bc;
-    int64_t *tco = tcy + P.bc;  // [BN]
-    T *cs = (T *)(tco + BN);    // ring [D][RP], then the staged outputs [JB][pitch]
+    // box tables, double-buffered: the next box's are built while this box's
+    // outputs are written.  tab[b] = tax[ba] tcx[ba] tay[bc] tcy[bc]
+    int64_t *tab0 = (int64_t *)(Bm + JB * ldb);
+    const int tabn = 2 * (P.ba + P.bc);
+    int64_t *tco = tab0 + 2 * tabn;       // [BN] C offset of position n (along-j stores)
+    T *ringbuf = (T *)(tco + BN);         // [D][RP]
+    T *cs = ringbuf + D * RP;             // [JB][pitch] staged outputs (not aliased: the next box's loads are in flight)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const T *A = (const T *)P.a;
     const T *B = (const T *)P.bm;
     T *C = (T *)P.c;
-    uint32_t tx, ty;
-    P.nx_div.divmod(blockIdx.x, ty, tx);
-    // this thread's own column first (registers only), so its loads are in
-    // flight while the matrix image and the box tables are built
     const int xl = tid & (P.ba - 1), yl = tid >> P.ba_shift;
-    int64_t ax = -1, cx = 0, ay = -1, cy = 0;
-    {
+    const int64_t I = P.I;
+    const int pitch = P.pitch;
+    const bool along_y = P.store == kFewAlongY;
+    const int64_t js = P.jstride;
+
+    // this thread's own column of a box (registers only), and its ring loads
+    int64_t ax, cx, ay, cy;
+    bool ok;
+    const T *pn;
+    int left;
+    auto own_column = [&](uint32_t tile) {
+        uint32_t tx, ty;
+        P.nx_div.divmod(tile, ty, tx);
+        ax = -1, cx = 0, ay = -1, cy = 0;
         const uint64_t x = (uint64_t)tx * P.ba + xl, y = (uint64_t)ty * P.bc + yl;
         if (x < P.X) few_decode((uint32_t)x, P.nxd, P.xdiv, P.xa, P.xc, ax, cx);
         if (y < P.Y) few_decode((uint32_t)y, P.nyd, P.ydiv, P.ya, P.yc, ay, cy);
-    }
-    const bool ok = ax >= 0 && ay >= 0;
-    const T *pn = A + (ok ? ax + ay : 0);  // masked positions read (and discard) column 0
-    const int64_t I = P.I;
-    double acc[MT][4][4];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int n = 0; n < 4; ++n)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[i][n][v] = 0.0;
-
-    T *ring = cs + tid;  // this thread's column
-    int left = K;        // rows not yet issued
+        ok = ax >= 0 && ay >= 0;
+        pn = A + (ok ? ax + ay : 0);  // masked positions read (and discard) column 0
+        left = K;
+    };
+    T *ring = ringbuf + tid;
     auto issue = [&](int half) {
         T *dst = ring + half * (H * RP);
         if (left >= H) {
@@ -348,100 +349,131 @@ __global__ void __launch_bounds__(kFewThreads) ttm_few_dmma_kernel(const __grid_
         left -= H;
         cp_async_commit();
     };
+    auto build_tables = [&](uint32_t tile, int64_t *tb) {
+        // x entries are the own columns of threads 0..ba-1; y entries are decoded
+        uint32_t tx, ty;
+        P.nx_div.divmod(tile, ty, tx);
+        if (tid < P.ba) {
+            tb[tid] = ax;
+            tb[P.ba + tid] = cx;
+        }
+        if (tid < P.bc) {
+            const uint64_t y = (uint64_t)ty * P.bc + tid;
+            int64_t oa = -1, oc = 0;
+            if (y < P.Y) few_decode((uint32_t)y, P.nyd, P.ydiv, P.ya, P.yc, oa, oc);
+            tb[2 * P.ba + tid] = oa;
+            tb[2 * P.ba + P.bc + tid] = oc;
+        }
+    };
+
+    uint32_t tile = blockIdx.x;
+    own_column(tile);
     issue(0);
     issue(1);
     for (int m = warp; m < JB; m += kFewThreads / 32)
         for (int k = lane; k < ldb; k += 32) Bm[m * ldb + k] = (m < J && k < K) ? (double)B[m * P.bs0 + k * P.bs1] : 0.0;
-    if (tid < P.ba) {
-        tax[tid] = ax;
-        tcx[tid] = cx;
-    }
-    if (tid < P.bc) {
-        const uint64_t y = (uint64_t)ty * P.bc + tid;
-        int64_t oa = -1, oc = 0;
-        if (y < P.Y) few_decode((uint32_t)y, P.nyd, P.ydiv, P.ya, P.yc, oa, oc);
-        tay[tid] = oa;
-        tcy[tid] = oc;
-    }
+    build_tables(tile, tab0);
     __syncthreads();
-    int half = 0;
-    const T *frag = cs + warp * 32 + g;  // + (k row) * RP + n8 tile * 8
-    for (int k0 = 0; k0 < K; k0 += H) {
-        cp_async_wait<1>();
-        __syncwarp();
-        const T *src = frag + half * (H * RP);
-        double bf[H / 4][4];
+    int cur = 0;
+    const T *frag = ringbuf + warp * 32 + g;  // + (k row) * RP + n8 tile * 8
+    for (;;) {
+        double acc[MT][4][4];
 #pragma unroll
-        for (int s = 0; s < H / 4; ++s)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) bf[s][n] = (k0 + 4 * s < K) ? (double)src[(4 * s + t) * RP + n * 8] : 0.0;
-        __syncwarp();  // every lane holds its fragments: the half can be refilled
-        issue(half);
+            for (int n = 0; n < 4; ++n)
 #pragma unroll
-        for (int s = 0; s < H / 4; ++s) {
-            if (k0 + 4 * s < K) {
-                const double *bm = Bm + g * ldb + k0 + 4 * s + t;
+                for (int v = 0; v < 4; ++v) acc[i][n][v] = 0.0;
+        int half = 0;
+        for (int k0 = 0; k0 < K; k0 += H) {
+            cp_async_wait<1>();
+            __syncwarp();
+            const T *src = frag + half * (H * RP);
+            double bf[H / 4][4];
 #pragma unroll
-                for (int i = 0; i < MT; ++i) {
-                    const double a0 = bm[(16 * i) * ldb], a1 = bm[(16 * i + 8) * ldb];
+            for (int s = 0; s < H / 4; ++s)
 #pragma unroll
-                    for (int n = 0; n < 4; ++n) few_mma(acc[i][n], a0, a1, bf[s][n]);
+                for (int n = 0; n < 4; ++n) bf[s][n] = (k0 + 4 * s < K) ? (double)src[(4 * s + t) * RP + n * 8] : 0.0;
+            __syncwarp();  // every lane holds its fragments: the half can be refilled
+            issue(half);
+#pragma unroll
+            for (int s = 0; s < H / 4; ++s) {
+                if (k0 + 4 * s < K) {
+                    const double *bm = Bm + g * ldb + k0 + 4 * s + t;
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const double a0 = bm[(16 * i) * ldb], a1 = bm[(16 * i + 8) * ldb];
+#pragma unroll
+                        for (int n = 0; n < 4; ++n) few_mma(acc[i][n], a0, a1, bf[s][n]);
+                    }
+                }
+            }
+            half ^= 1;
+        }
+        // this box's C offsets before the next box's column replaces them
+        const int64_t my_co = ok ? cx + cy : -1;
+        const int64_t *tb = tab0 + cur * tabn;
+        // the ring is drained: put the next box's loads in flight before
+        // this box is staged and written
+        const uint32_t next = tile + gridDim.x;
+        const bool more = next < P.ntiles;
+        if (more) {
+            own_column(next);
+            issue(0);
+            issue(1);
+        }
+        // fragments -> staged tile cs[j][pos]: row j = 16 i + g + 8 h, column n = 32 warp + 8 n8 + 2 t + v
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int col = warp * 32 + n * 8 + 2 * t + v;
+                const int pos = along_y ? (col >> P.ba_shift) * (P.ba + 1) + (col & (P.ba - 1)) : col;
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) cs[(16 * i + g + 8 * h) * pitch + pos] = (T)acc[i][n][2 * h + v];
+            }
+        }
+        if (P.store == kFewAlongJ) tco[tid] = my_co;
+        if (more) build_tables(next, tab0 + (cur ^ 1) * tabn);
+        __syncthreads();
+        if (P.store != kFewAlongJ) {
+            // a thread keeps one position of the box for every j: lanes along y
+            // (C's fastest free direction) or, for direct boxes, along x
+            int xx = xl, yy = yl, pos = tid;
+            if (along_y) {
+                yy = tid & (P.bc - 1);
+                xx = tid >> P.bc_shift;
+                pos = yy * (P.ba + 1) + xx;
+            }
+            if (tb[xx] >= 0 && tb[2 * P.ba + yy] >= 0) {
+                T *pc = C + tb[P.ba + xx] + tb[2 * P.ba + P.bc + yy];
+                const T *src = cs + pos;
+#pragma unroll
+                for (int j = 0; j < JB; ++j) {
+                    if (j < J) *pc = src[j * pitch];
+                    pc += js;
+                }
+            }
+        } else {
+            // C contiguous along j: lanes write each position's J-run
+            const int j = tid % JB;
+            if (j < J) {
+                const T *src = cs + j * pitch;
+#pragma unroll 4
+                for (int n = tid / JB; n < BN; n += kFewThreads / JB) {
+                    const int64_t co = tco[n];
+                    if (co >= 0) C[co + j] = src[n];
                 }
             }
         }
-        half ^= 1;
+        if (!more) break;
+        __syncthreads();  // the staged tile and tco are free for the next box
+        tile = next;
+        cur ^= 1;
     }
     cp_async_wait<0>();
-    __syncthreads();  // every warp is done with the ring (the staged tile aliases it)
-
-    // fragments -> staged tile cs[j][pos]: row j = 16 i + g + 8 h, column n = 32 warp + 8 n8 + 2 t + v
-    const int pitch = P.pitch;
-    const bool along_y = P.store == kFewAlongY;
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            const int col = warp * 32 + n * 8 + 2 * t + v;
-            const int pos = along_y ? (col >> P.ba_shift) * (P.ba + 1) + (col & (P.ba - 1)) : col;
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) cs[(16 * i + g + 8 * h) * pitch + pos] = (T)acc[i][n][2 * h + v];
-        }
-    }
-    if (P.store == kFewAlongJ) tco[tid] = ok ? cx + cy : -1;
-    __syncthreads();
-    const int64_t js = P.jstride;
-    if (P.store != kFewAlongJ) {
-        // a thread keeps one position of the box for every j: lanes along y
-        // (C's fastest free direction) or, for direct boxes, along x
-        int xx = xl, yy = yl, pos = tid;
-        if (along_y) {
-            yy = tid & (P.bc - 1);
-            xx = tid >> P.bc_shift;
-            pos = yy * (P.ba + 1) + xx;
-        }
-        if (tax[xx] < 0 || tay[yy] < 0) return;
-        T *pc = C + tcx[xx] + tcy[yy];
-        const T *src = cs + pos;
-#pragma unroll
-        for (int j = 0; j < JB; ++j) {
-            if (j < J) *pc = src[j * pitch];
-            pc += js;
-        }
-        return;
-    }
-    {
-        // C contiguous along j: lanes write each position's J-run
-        const int j = tid % JB;
-        if (j >= J) return;
-        const T *src = cs + j * pitch;
-#pragma unroll 4
-        for (int n = tid / JB; n < BN; n += kFewThreads / JB) {
-            const int64_t co = tco[n];
-            if (co >= 0) C[co + j] = src[n];
-        }
-    }
 }
 
 // ------------------------------------------------------------------ planning
@@ -592,10 +624,20 @@ static bool plan_few(const tl_desc &a, const void *a_ptr, const tl_desc &bm, con
     fp.jb = jb;
     fp.dmma = dmma;
     fp.mt = mt;
+    P.ntiles = (uint32_t)(nX * nY);
     fp.grid = nX * nY;
-    const size_t ring = (size_t)kFewRing * (dmma ? kFewRingPitch : BN) * es;
-    const size_t stage = dmma ? (size_t)16 * mt * P.pitch * es : (store == kFewDirect ? 0 : (size_t)jb * P.pitch * es);
-    fp.smem = bbytes + (size_t)2 * (ba + bc) * 8 + (size_t)BN * 8 + std::max(ring, stage);
+    if (dmma) {
+        // persistent CTAs: ring and staged tile side by side, two table sets
+        const size_t ring = (size_t)kFewRing * kFewRingPitch * es, stage = (size_t)16 * mt * P.pitch * es;
+        fp.smem = bbytes + (size_t)4 * (ba + bc) * 8 + (size_t)BN * 8 + ring + stage;
+        const DeviceInfo &di = device_info();
+        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(mt == 1 ? 6 : 4, (224 * 1024) / (int64_t)(fp.smem + 1024)));
+        fp.grid = std::min<int64_t>(fp.grid, (int64_t)di.num_sms * per_sm);
+    } else {
+        const size_t ring = (size_t)kFewRing * BN * es;
+        const size_t stage = store == kFewDirect ? 0 : (size_t)jb * P.pitch * es;
+        fp.smem = bbytes + (size_t)2 * (ba + bc) * 8 + (size_t)BN * 8 + std::max(ring, stage);
+    }
     return fp.smem <= 150 * 1024;
 }
 

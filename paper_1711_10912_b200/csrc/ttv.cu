@@ -1177,7 +1177,10 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
     using Acc = typename AccOf<TA>::type;
     constexpr int KC = 128 / (int)sizeof(TA);  // elements per 128-byte slab row
     constexpr int E = 16 / (int)sizeof(TA);    // elements per 16-byte chunk
-    constexpr int STAGE = kRowsTmaR * 128;     // bytes
+    // rows per tile = threads per CTA (256, 128 or 64: chosen by the planner so
+    // that the tiles fill whole rounds of the persistent grid)
+    const int RT = (int)blockDim.x;
+    const int STAGE = RT * 128;  // bytes
     extern __shared__ __align__(16) unsigned char smem_raw[];  // stages are re-aligned to 1024 below
     __shared__ __align__(8) uint64_t full_bar[kRowsTmaStages];
     pdl_wait();
@@ -1193,7 +1196,7 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
     }
     __syncthreads();
     const int nslab = (int)((K + KC - 1) / KC);
-    const int64_t ntiles = (P.O + kRowsTmaR - 1) / kRowsTmaR;
+    const int64_t ntiles = (P.O + RT - 1) / RT;
     const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t nitems = my_tiles * nslab;
     int64_t p_tile = blockIdx.x;
@@ -1209,10 +1212,10 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&full_bar[p_stage], STAGE);
             if (keep)
-                tma_load_2d_hint(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * kRowsTmaR), &full_bar[p_stage],
+                tma_load_2d_hint(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * RT), &full_bar[p_stage],
                                  p_tile >= P.keep_tile ? pol_keep : pol_first);
             else
-                tma_load_2d(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * kRowsTmaR), &full_bar[p_stage]);
+                tma_load_2d(stages + p_stage * STAGE, &map, p_slab * KC, (int32_t)(p_tile * RT), &full_bar[p_stage]);
         }
         if (++p_slab == nslab) {
             p_slab = 0;
@@ -1252,7 +1255,7 @@ __global__ void __launch_bounds__(kRowsTmaR) ttv_rows_tma_kernel(const __grid_co
             }
         }
         if (slab == nslab - 1) {
-            const int64_t o = tile * kRowsTmaR + r;
+            const int64_t o = tile * RT + r;
             if (o < P.O) {
                 const int64_t off = P.ident ? o : P.out_map.map((uint32_t)o);
                 ((TC *)P.c)[off] = narrow<TC>(acc);
@@ -1589,21 +1592,51 @@ static bool plan_rows_tma(TtvLaunch &L, const Canon &cn, int32_t dtype, int nsm)
     if (cn.O < kRowsTmaR) return false;
     PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
     if (enc == nullptr) return false;
+    // Rows per tile R (= threads per CTA) and CTAs per SM: the persistent
+    // grid walks the tiles in rounds, so 625 tiles on 296 CTAs (400^3
+    // float64, R = 256) take 3 rounds for 2.1 rounds of work (measured 0.835
+    // of HBM).  Pick the (R, CTAs per SM) whose last round is fullest; within
+    // 2% prefer the larger tile.
+    const size_t bbytes = (((size_t)cn.K * 8 + 15) & ~(size_t)15);
+    int bestR = kRowsTmaR, best_ps = 1;
+    double best_eff = -1.0;
+    static const int fixedR = [] {
+        const char *e = getenv("TL_TTV_ROWS_R");  // 256 / 128 / 64: fixed rows per tile (0 = choose)
+        return e ? atoi(e) : 0;
+    }();
+    for (int R : {256, 128, 64}) {
+        if (fixedR != 0 && R != fixedR) continue;
+        const size_t smem = 1024 + (size_t)kRowsTmaStages * R * 128 + bbytes;
+        if (smem > 200 * 1024) continue;
+        const int64_t tiles = (cn.O + R - 1) / R;
+        const int max_ps = (int)std::max<int64_t>(1, std::min<int64_t>(R == 256 ? 2 : R == 128 ? 4 : 8, (228 * 1024) / ((int64_t)smem + 2048)));
+        for (int ps = max_ps; ps >= 1; --ps) {
+            // enough rows in flight per SM to hide the loads (one 64-thread CTA per SM measured 2x slower)
+            if (R * ps < 384 && ps < max_ps) break;
+            const int64_t slots = std::min<int64_t>(tiles, (int64_t)nsm * ps);
+            const int64_t rounds = (tiles + slots - 1) / slots;
+            const double eff = (double)tiles / (double)(rounds * slots);
+            if (eff > best_eff + 0.02) {
+                best_eff = eff;
+                bestR = R;
+                best_ps = ps;
+            }
+        }
+    }
+    if (best_eff < 0) return false;
     const cuuint64_t dims[2] = {(cuuint64_t)cn.K, (cuuint64_t)cn.O};
     const cuuint64_t strides[1] = {(cuuint64_t)(cn.K * s)};
-    const cuuint32_t box[2] = {(cuuint32_t)(128 / s), (cuuint32_t)kRowsTmaR};
+    const cuuint32_t box[2] = {(cuuint32_t)(128 / s), (cuuint32_t)bestR};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&L.tmap, dtype == TL_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                      (void *)P.a, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     L.rows_tma = true;
-    L.block = dim3(kRowsTmaR);
-    L.smem = 1024 + (size_t)kRowsTmaStages * kRowsTmaR * 128 + (((size_t)cn.K * 8 + 15) & ~(size_t)15);
-    if (L.smem > 200 * 1024) return false;
-    const int64_t ntiles = (cn.O + kRowsTmaR - 1) / kRowsTmaR;
-    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / ((int64_t)L.smem + 2048)));
-    L.grid = dim3((unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * per_sm));
+    L.block = dim3(bestR);
+    L.smem = 1024 + (size_t)kRowsTmaStages * bestR * 128 + bbytes;
+    const int64_t ntiles = (cn.O + bestR - 1) / bestR;
+    L.grid = dim3((unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * best_ps));
     return true;
 }
 
@@ -2396,8 +2429,9 @@ int ttv_enqueue(const tl_desc &a, const void *a_ptr, const void *b_ptr, int32_t 
             L.keep_bytes = in_keep;  // split into keep_k / keep_cta at launch (needs the occupancy)
         } else if (L.rows_tma) {
             P.l2_stream = 1;
-            const int64_t ntiles = (P.O + kRowsTmaR - 1) / kRowsTmaR;
-            P.keep_tile = ntiles - std::min<int64_t>(ntiles, in_keep / (kRowsTmaR * P.K * s));
+            const int64_t rt = (int64_t)L.block.x;  // rows per tile
+            const int64_t ntiles = (P.O + rt - 1) / rt;
+            P.keep_tile = ntiles - std::min<int64_t>(ntiles, in_keep / (rt * P.K * s));
         }
     }
     if (L.regime == 5) return ttv_short_run(L, a.dtype, c_dtype, c_ptr, st);

@@ -231,7 +231,7 @@ template <class T, int VEC> __device__ __forceinline__ void load_vec(const T *p,
     }
 }
 
-template <class TA, class TB, int VEC, bool SAME, int U = 4, bool FMA_ACC = false>
+template <class TA, class TB, int VEC, bool SAME, int U = 4, bool FMA_ACC = false, bool ROWV = false>
 __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ ReduceParams P) {
     using Acc = typename RedAcc<TA>::type;
     typename std::conditional<FMA_ACC, FmaAcc, ThreadAcc<TA>>::type ta;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256) dot_rows_kernel(const __grid_constant__ R
             }
         }
         for (int64_t e = nv * VEC + tid; e < L; e += nthreads) ta.add(0, as_acc(a[e]), as_acc(b[e]));
-    } else if (VEC > 1 && P.row_vec) {
+    } else if (ROWV && VEC > 1 && P.row_vec) {
         // rows along the shared fastest dimension, in a different order in b
         // (e.g. layouts (1,2,3,4) x (1,4,2,3)): 16-byte vectors, U in flight
         // per thread and operand, row starts through b's digit map
@@ -718,6 +718,7 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         const unsigned G = (unsigned)grid;
         if (a.dtype == TL_F32 && b.dtype == TL_F32) {
             if (same && al) dot_rows_kernel<float, float, 4, true, 8><<<G, threads, 0, st>>>(P);  // 8 x 16 B in flight: one stream
+            else if (al && P.row_vec) dot_rows_kernel<float, float, 4, false, 4, false, true><<<G, threads, 0, st>>>(P);
             else if (al) dot_rows_kernel<float, float, 4, false><<<G, threads, 0, st>>>(P);
             else dot_rows_kernel<float, float, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F64 && b.dtype == TL_F64) {
@@ -725,6 +726,7 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
             const bool fma_ok = (N + (int64_t)G * threads * 4 - 1) / ((int64_t)G * threads * 4) <= kFmaChain;
             if (same && al && fma_ok) dot_rows_kernel<double, double, 2, true, 8, true><<<G, threads, 0, st>>>(P);
             else if (same && al) dot_rows_kernel<double, double, 2, true, 8><<<G, threads, 0, st>>>(P);
+            else if (al && P.row_vec) dot_rows_kernel<double, double, 2, false, 4, false, true><<<G, threads, 0, st>>>(P);
             else if (al) dot_rows_kernel<double, double, 2, false><<<G, threads, 0, st>>>(P);
             else dot_rows_kernel<double, double, 1, false><<<G, threads, 0, st>>>(P);
         } else if (a.dtype == TL_F32 && b.dtype == TL_F64) {
@@ -732,7 +734,8 @@ int reduce_enqueue(const tl_desc &a, const void *a_ptr, const tl_desc &b, const 
         } else if (a.dtype == TL_F64 && b.dtype == TL_F32) {
             dot_rows_kernel<double, float, 1, false><<<G, threads, 0, st>>>(P);
         } else {
-            if (al) dot_rows_kernel<int64_t, int64_t, 2, false><<<G, threads, 0, st>>>(P);
+            if (al && P.row_vec) dot_rows_kernel<int64_t, int64_t, 2, false, 4, false, true><<<G, threads, 0, st>>>(P);
+            else if (al) dot_rows_kernel<int64_t, int64_t, 2, false><<<G, threads, 0, st>>>(P);
             else dot_rows_kernel<int64_t, int64_t, 1, false><<<G, threads, 0, st>>>(P);
         }
         e = cudaGetLastError();

@@ -14,15 +14,19 @@
 // Odd extents need no divisibility: x and y are flattened over whole digit
 // groups and only the last box of each group is masked.
 //
-// Each thread folds one position for all J rows at once (J accumulators per
-// position, B in shared memory as [k][j]; k in order, so every output is the
-// same chain as in the other ttm kernels: fused multiply-add for float64 --
-// the DMMA semantics --, exact for float32 (products are exact in binary64)
-// and int64).  A is read with L1-allocating loads: when the run along x is
-// shorter than a sector (small inner blocks, contracted stride 1), the rest of
-// the sector is consumed by the same CTA a few k-steps later.  Outputs are
-// staged in shared memory and written along C (y fastest), along j when C is
-// contiguous in j, or directly when x is C's fastest direction too.
+// Each thread streams the column of one position (its K elements, I apart)
+// through a private ring of k-rows in shared memory (cp.async.ca: when the run
+// along x is shorter than a sector -- small inner blocks, contracted stride 1
+// -- L1 keeps the rest of the sector for the neighbouring rows).  Two folds,
+// both in k order with fused multiply-adds, so every output is the same chain
+// as in the stream / bulk / GETT kernels (exact for float32, whose products
+// are exact in binary64, and for int64):
+//   * ttm_few_dmma_kernel (float64 / float32, K >= 9): FP64 tensor cores, a
+//     warp = 4 n8 tiles of positions, persistent CTAs;
+//   * ttm_few_kernel (K <= 8, int64): J accumulators per thread, b(., k)
+//     broadcast from shared memory.
+// Outputs are staged in shared memory and written along C (y fastest), along
+// j when C is contiguous in j, or along x when x is C's fastest direction too.
 #include <algorithm>
 #include <cstdlib>
 #include <string>

@@ -1983,10 +1983,19 @@ static bool plan_tile(const Canon &cn, TtvLaunch &L, int nsm, bool s8) {
     int c0 = 0;
     for (size_t q = 1; q < nf; ++q)
         if (F[q].cs < F[c0].cs) c0 = (int)q;
+    // A chain extent that leaves a ragged last block (33 in blocks of 32: half
+    // the tile idle; 85 in blocks of 64: a third) is flattened together with
+    // further digits -- the chains are plain mixed-radix index spaces (the
+    // kernel decodes A and C offsets per position), so the digits need not be
+    // contiguous: runs simply end where a digit wraps.  TL_TTV_TILE_RAGGED=0:
+    // the contiguous chains only.
+    static const bool fill = getenv("TL_TTV_TILE_RAGGED") == nullptr || atoi(getenv("TL_TTV_TILE_RAGGED")) != 0;
+    auto ragged = [&](int64_t e, int t) { return fill && (double)((e + t - 1) / t * t) > 1.15 * (double)e; };
     std::vector<int> ych;
     int64_t ey = 1;
-    for (size_t q = 0; q < nf && ey < ty && (int)q != c0; ++q) {
-        if (q == cn.inner.size() && ey >= 16) break;  // do not cross the k gap once Y is usable
+    for (size_t q = 0; q < nf && (ey < ty || ragged(ey, ty)) && (int)q != c0; ++q) {
+        // do not cross the k gap once Y is usable (unless its last block is ragged)
+        if (q == cn.inner.size() && ey >= 16 && !ragged(ey, ty)) break;
         ych.push_back((int)q);
         used[q] = 1;
         ey *= F[q].ext;
@@ -2008,6 +2017,16 @@ static bool plan_tile(const Canon &cn, TtvLaunch &L, int nsm, bool s8) {
             for (size_t q = 0; q < nf; ++q)
                 if (!used[q] && F[q].cs == last.cs * last.ext) nxt = (int)q;
             if (nxt < 0) break;
+            xch.push_back(nxt);
+            used[nxt] = 1;
+            ex *= F[nxt].ext;
+        }
+        // ragged or short: continue with the remaining digits in C order
+        while (fill && (ex < tx || ragged(ex, tx))) {
+            int nxt = -1;
+            for (size_t q = 0; q < nf; ++q)
+                if (!used[q] && (nxt < 0 || F[q].cs < F[nxt].cs)) nxt = (int)q;
+            if (nxt < 0 || ex * F[nxt].ext > 0x7fffffffll) break;
             xch.push_back(nxt);
             used[nxt] = 1;
             ex *= F[nxt].ext;

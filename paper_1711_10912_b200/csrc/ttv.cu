@@ -2181,7 +2181,17 @@ static int ttv_make_plan(const tl_desc &a, const void *a_ptr, int m0, TtvLaunch 
         return TL_OK;
     }
     // (K <= 4: from K ~ 9 the boxed / staged kernels do better, config 5)
-    if (allow_short && short_min > 0 && P.K <= 4 && !cn.ident && P.O * P.K * P.I * (int64_t)s >= short_min &&
+    // (with the flattened chains also K <= 8 on the strided regime, I >= 32:
+    //  K = 5 on the config-5 shape 275-489 -> 234-424 us, K = 6, I = 88760 of
+    //  the random sweep 2167 -> 279 us; with I < 32 the staged tiles were mixed
+    //  -- 405 -> 258 but 215 -> 537 and 196 -> 429 us -- and are kept; from
+    //  K = 9 the boxed / strided kernels win)
+    static const int64_t tile_max_k = [] {
+        const char *e = getenv("TL_TTV_TILE_MAXK");
+        return (int64_t)(e ? atoll(e) : 8);
+    }();
+    if (allow_short && short_min > 0 && (P.K <= 4 || (P.K <= tile_max_k && P.I >= 32)) && !cn.ident &&
+        P.O * P.K * P.I * (int64_t)s >= short_min &&
         a.dtype != TL_I64 && plan_tile(cn, L, di.num_sms, s == 8))
         return TL_OK;
     const size_t small_bbytes = ((size_t)P.K * 8 + 15) & ~(size_t)15;

@@ -1882,6 +1882,25 @@ static bool plan_box(const Canon &cn, TtvLaunch &L, int64_t s, uintptr_t base_ad
         chain.push_back(nxt);
         cext *= free[nxt].ext;
     }
+    // a short or ragged C-chain (its last block of 64 mostly idle) continues
+    // over the remaining digits in C order -- the chain is a flat index space
+    // decoded per position, so the digits need not be C-contiguous; only
+    // digits the A-chain does not need (TL_TTV_BOX_RAGGED=0: contiguous only)
+    {
+        static const bool fill = getenv("TL_TTV_BOX_RAGGED") == nullptr || atoi(getenv("TL_TTV_BOX_RAGGED")) != 0;
+        const size_t na0 = d0.ext >= 16 ? 1 : ninner;
+        auto ragged = [&](int64_t e) { return (double)((e + 63) / 64 * 64) > 1.15 * (double)e; };
+        while (fill && (cext < 64 || ragged(cext)) && (int)chain.size() < kBoxMaxChain) {
+            int nxt = -1;
+            for (size_t q = na0; q < free.size(); ++q) {
+                if (std::find(chain.begin(), chain.end(), (int)q) != chain.end()) continue;
+                if (nxt < 0 || free[q].cs < free[nxt].cs) nxt = (int)q;
+            }
+            if (nxt < 0 || cext * free[nxt].ext > 0x7fffffffll) break;
+            chain.push_back(nxt);
+            cext *= free[nxt].ext;
+        }
+    }
     if (cext < 16 || cext > 0xffffffffll) return false;
     // A-chain: inner digits [0, na) -- d0 alone when it is long enough (the
     // tuned one-digit box), else as many inner digits as precede the C-chain

@@ -2012,7 +2012,14 @@ static bool plan_tile(const Canon &cn, TtvLaunch &L, int nsm, bool s8) {
     auto ragged = [&](int64_t e, int t) { return fill && (double)((e + t - 1) / t * t) > 1.15 * (double)e; };
     std::vector<int> ych;
     int64_t ey = 1;
-    for (size_t q = 0; q < nf && (ey < ty || ragged(ey, ty)) && (int)q != c0; ++q) {
+    for (size_t q = 0; q < nf && (ey < ty || ragged(ey, ty)); ++q) {
+        if ((int)q == c0) {
+            // the C-fastest digit heads the X chain.  When it is also A's
+            // fastest digit (a tiny one, e.g. extent 3: longer ones took the
+            // short-fold stream) Y continues behind it; else Y ends here
+            if (fill && q == 0) continue;
+            break;
+        }
         // do not cross the k gap once Y is usable (unless its last block is ragged)
         if (q == cn.inner.size() && ey >= 16 && !ragged(ey, ty)) break;
         ych.push_back((int)q);

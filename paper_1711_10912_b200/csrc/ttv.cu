@@ -1378,6 +1378,17 @@ static bool plan_staged(TtvLaunch &L, int64_t s, uintptr_t base_addr, int nsm) {
     int64_t R;
     if (I == 1) {
         R = threads;
+        // rows that are not whole 16-byte vectors (K = 33 doubles = 264 bytes)
+        // would be copied in 8-byte cp.async pieces (measured 0.47 of HBM);
+        // with fewer rows per tile the whole tile is one contiguous, 16-byte
+        // aligned range that fits a stage and streams as ONE TMA bulk copy
+        // (TL_TTV_ROWS_BULK=0: off)
+        static const bool rows_bulk = getenv("TL_TTV_ROWS_BULK") == nullptr || atoi(getenv("TL_TTV_ROWS_BULK")) != 0;
+        if (rows_bulk && (K * s) % 16 != 0 && base_addr % 16 == 0 && K % 2 == 1 && 32 * K * s <= 32 * 1024) {
+            int64_t r = std::min<int64_t>(256, (32 * 1024) / (K * s) / 32 * 32);
+            while (r >= 32 && (r * K * s) % 16 != 0) r -= 32;
+            if (r >= 32) R = r;
+        }
         // small problems: fewer rows per tile so every SM gets a tile
         while (R > 32 && (O + R - 1) / R < nsm) R /= 2;
         threads = (int)std::max<int64_t>(32, R);

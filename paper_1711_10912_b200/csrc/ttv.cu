@@ -2025,10 +2025,10 @@ static bool plan_tile(const Canon &cn, TtvLaunch &L, int nsm, bool s8) {
     int64_t ey = 1;
     for (size_t q = 0; q < nf && (ey < ty || ragged(ey, ty)); ++q) {
         if ((int)q == c0) {
-            // the C-fastest digit heads the X chain.  When it is also A's
-            // fastest digit (a tiny one, e.g. extent 3: longer ones took the
-            // short-fold stream) Y continues behind it; else Y ends here
-            if (fill && q == 0) continue;
+            // the C-fastest digit heads the X chain; a Y chain that is still
+            // short or ragged continues behind it (e.g. when it is also A's
+            // fastest digit, a tiny one: longer ones took the short-fold stream)
+            if (fill) continue;
             break;
         }
         // do not cross the k gap once Y is usable (unless its last block is ragged)

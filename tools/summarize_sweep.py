@@ -81,3 +81,33 @@ def main(tag):
 
 if __name__ == "__main__":
     main(sys.argv[1] if len(sys.argv) > 1 else "r05")
+
+
+def layout_sweep_md(tag, seeds=(7, 11)):
+    """profiles/layout_sweep_<tag>.md from gpurun_out/layout_sweep_<tag>_<seed>.jsonl (tools/experiments/layout_sweep.py)."""
+    import re
+    md = [f"# Random-layout ttv sweep ({tag})", "",
+          "`tools/experiments/layout_sweep.py 24 SEED`: random order 2-7, extents 2..10^6 with ~512 MB per tensor (float32 /",
+          "float64 alternating), random permutation layout, every mode; ttv timed by graph replays; fraction of the pod's",
+          "measured HBM copy peak for algorithmic bytes. Same seeds and cases as `layout_sweep_r04.md` (whose 'after' rows are",
+          "the start of this comparison).", "",
+          "| run | ttvs | p10 | p25 | median | p75 | >= 0.8 | < 0.5 |", "|---|---|---|---|---|---|---|---|"]
+    allrows = []
+    for sd in seeds:
+        path = os.path.join(OUT, f"layout_sweep_{tag}_{sd}.jsonl")
+        rows = [json.loads(l) for l in open(path) if '"case"' in l]
+        allrows += rows
+        fr = sorted(r["frac"] for r in rows)
+        q = lambda p: fr[int(p * (len(fr) - 1))]
+        md.append(f"| seed {sd} | {len(fr)} | {q(0.1):.3f} | {q(0.25):.3f} | {statistics.median(fr):.3f} | {q(0.75):.3f} | "
+                  f"{sum(f >= 0.8 for f in fr)} | {sum(f < 0.5 for f in fr)} |")
+    md += ["", "Both seeds, by kernel:", "", "| kernel | ttvs | min | median | max |", "|---|---|---|---|---|"]
+    by = {}
+    for r in allrows:
+        by.setdefault(r["kernel"].split(" ")[0], []).append(r["frac"])
+    for k, v in sorted(by.items(), key=lambda kv: -statistics.median(kv[1])):
+        v.sort()
+        md.append(f"| {k} | {len(v)} | {v[0]:.3f} | {statistics.median(v):.3f} | {v[-1]:.3f} |")
+    md.append("")
+    open(os.path.join(ROOT, "profiles", f"layout_sweep_{tag}.md"), "w").write("\n".join(md) + "\n")
+    print("\n".join(md))

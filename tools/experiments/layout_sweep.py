@@ -54,9 +54,21 @@ def main():
         layout = tuple(int(x) + 1 for x in rng.permutation(p))
         n = int(np.prod(shape))
         buf = torch.rand(n, dtype=dtype, device="cuda")
-        A = tl.DenseTensor._wrap(TensorMeta(shape, layout=layout), buf)
+        check = os.environ.get("TL_SWEEP_CHECK") is not None
+        if check:
+            # the same logical tensor in first-order layout: every ttv output must be bit-identical
+            A0 = tl.DenseTensor._wrap(TensorMeta(shape), buf)
+            A = tl.DenseTensor._wrap(TensorMeta(shape), buf.clone())
+            A.relayout(layout)
+        else:
+            A = tl.DenseTensor._wrap(TensorMeta(shape, layout=layout), buf)
         for mode in range(1, p + 1):
             v = tl.DenseTensor._wrap(TensorMeta((shape[mode - 1],)), torch.rand(shape[mode - 1], dtype=dtype, device="cuda"))
+            if check:
+                same = bool(torch.equal(tl.ttv(A, v, mode).buffer, tl.ttv(A0, v, mode).buffer))
+                if not same:
+                    print(json.dumps({"MISMATCH": True, "shape": shape, "layout": layout, "mode": mode}), flush=True)
+                    raise SystemExit(1)
             us = timeit(lambda: tl.ttv(A, v, mode), n=5)
             nbytes = s * (n + shape[mode - 1] + n // shape[mode - 1])
             info = ctypes.create_string_buffer(512)
@@ -72,6 +84,8 @@ def main():
             rows.append(row)
             print(json.dumps(row), flush=True)
         del A, buf
+        if check:
+            del A0
         torch.cuda.empty_cache()
     fr = [r["frac"] for r in rows]
     print(json.dumps({"summary": True, "cases": len(rows), "min_frac": min(fr), "median_frac": statistics.median(fr),

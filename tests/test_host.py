@@ -136,6 +136,27 @@ def test_ttv_plans_for_other_configs():
     assert plan(0, (400, 400), (1, 2), 2, _abi.TL_F64)["regime"] == "small-cols"
 
 
+def test_ttv_plans_on_the_config5_shape_round2():
+    """Planner rules added in round 2 ("The configs' own shapes"), on the
+    order-7 config-5 shape in layouts of the every-layout sweep."""
+    shape = (3, 33, 5, 17, 9, 2, 640)
+    # rows of 2 elements x 640 k-rows: the staged tiles with fewer rows per tile, not one thread per fibre
+    p = plan(0, shape, (6, 7, 3, 4, 5, 1, 2), 7, _abi.TL_F64)
+    assert (p["regime"], p["K"], p["I"]) == ("staged", 640, 2)
+    # unaligned rows (33 doubles = 264 bytes): 96 rows per tile stream as one TMA bulk copy
+    p = plan(0, shape, (2, 5, 3, 4, 7, 6, 1), 2, _abi.TL_F64)
+    assert (p["regime"], p["K"], p["I"], p["block"]) == ("staged-bulk", 33, 1, 96)
+    # short folds with scattered outputs: the tile-fold kernel with flattened chains -- also when the
+    # C-fastest digit is A's fastest one (extent 3), when a chain extent is ragged (33, 85), and for
+    # 4 < K <= 8 on the strided regime
+    for layout, mode, K, I in [((1, 6, 7, 3, 5, 2, 4), 6, 2, 3), ((6, 1, 2, 5, 3, 7, 4), 1, 3, 2),
+                               ((3, 4, 1, 6, 5, 2, 7), 1, 3, 85), ((2, 3, 1, 6, 5, 4, 7), 3, 5, 33)]:
+        p = plan(0, shape, layout, mode, _abi.TL_F64)
+        assert (p["regime"], p["K"], p["I"]) == ("tile-fold", K, I), (layout, mode, p)
+    # K = 9 (config 5's own mode) stays on the boxed / strided kernels
+    assert plan(0, shape, (7, 4, 2, 1, 6, 3, 5), 5, _abi.TL_F64)["regime"] in ("strided", "strided-box")
+
+
 def test_ttm_gett_plans():
     # config 3 on the GETT: operand majors and the free-digit order sigma
     p = plan(1, (512,) * 3, (1, 2, 3), 1, _abi.TL_F64, (384, 512))
